@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path of arXiv 2103.01597: RK3 substeps of FP64 MHD.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A bench "step" is one full RK3 step = 3 ISL iterations, each one pass of the whole
+hot path: self halo copy, pack -> NCCL exchange -> unpack (N > 1) overlapped with the inner
+update, outer update.  Metric (BASELINE.json): Gcell-updates/s per RK3 substep
+= global interior cells x substeps / time.
+
+Default workload: 256^3 FP64 per GPU (BASELINE configs[1] at N = 1; configs[3] weak scaling
+for N > 1: global grid = 256^3 x Morton partition, 512^3 at N = 8).  --scaling strong
+--grid 512 runs configs[2].  ICs: counter-based splitmix64 uniform [0, 1),
+dt = 1.19209e-7, parameters P0 (reading R#12).  Inputs (2.3 GB per GPU) are far
+larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gcell-updates/s per RK3 substep (FP64 MHD)"
+UNIT = "Gcell-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--grid", type=int, default=256, help="per-GPU n (weak) or global n (strong)")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak")
+    ap.add_argument("--dtype", choices=("f64", "f32"), default="f64")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 direct, 2 z-marching")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--corners", action="store_true")
+    return ap.parse_args()
+
+
+# ---- clocks during the timed region (B200_PROFILING.md clocks line) -------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.1)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        pw = [float(s[3]) for s in self.samples if s[3].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(self.samples), "reasons": reasons}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# FP64 issue peak measured on this pool's B200 with a DFMA microbenchmark
+# (tools/microbench/fp64_peak.cu, profiles/r01_fp64_lds_microbench.txt): 17.09 T DFMA-lane/s.
+FP64_PEAK_LANE_OPS = 17.09e12
+
+
+def cpu_baseline(n_glob, ds, params, dt, seconds_hint=True):
+    """The oracle as it stands, on the host cores: one RK3 step (3 substeps) of a 256 x 256 x 32
+    periodic slab of the bench workload (same cells, same per-cell work; bounded sample)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    nz = 32
+    st = synth.splitmix_state((n_glob[2], n_glob[1], n_glob[0]), (0, 0, 0), (nz, n_glob[1], n_glob[0]))
+    oracle.integrate(st[:, :8], ds, params, dt, 0, substeps=1)  # warm the thread pool
+    t0 = time.perf_counter()
+    oracle.integrate(st, ds, params, dt, 1)
+    el = time.perf_counter() - t0
+    cells = nz * n_glob[1] * n_glob[0]
+    return {"value": cells * 3 / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"1 RK3 step (3 substeps) of a {n_glob[0]}x{n_glob[1]}x{nz} periodic slab of the "
+                      f"workload, {el:.2f} s wall, OpenMP over z"}
+
+
+def run_reference(args, n_glob, rank):
+    """--impl reference: the oracle (the paper's 'single-core CPU solver logically equivalent',
+    P:899, here with OpenMP) as it stands, one bounded sample per step."""
+    import numpy as np
+
+    import oracle
+    import synth
+    if rank != 0:
+        return
+    ds = synth.spacing(n_glob)
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    nz = 16
+    st = synth.splitmix_state((n_glob[2], n_glob[1], n_glob[0]), (0, 0, 0), (nz, n_glob[1], n_glob[0]))
+    oracle.integrate(st[:, :4], ds, synth.P0, synth.DT, 0, substeps=1)
+    cur = st
+    for _ in range(args.warmup):
+        cur = oracle.integrate(cur, ds, synth.P0, synth.DT, 0, substeps=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cur = oracle.integrate(cur, ds, synth.P0, synth.DT, 0, substeps=1)
+    el = time.perf_counter() - t0
+    cells = nz * n_glob[1] * n_glob[0]
+    value = cells * args.steps / el / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{n_glob[0]}^3 FP64 MHD RK3 substep" if n_glob[0] == n_glob[1] == n_glob[2]
+                       else f"{n_glob} FP64 MHD RK3 substep", "grid": list(n_glob)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"per step: 1 substep of a {n_glob[0]}x{n_glob[1]}x{nz} periodic slab"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        args.gpus = world
+
+    # decomposition for the weak-scaling global grid
+    def morton_partition(nr):
+        P = [1, 1, 1]
+        v = nr - 1
+        k = 0
+        while v >> (3 * k):
+            for j in range(3):
+                P[2 - j] += ((v >> (3 * k + j)) & 1) << k
+            k += 1
+        return P  # (x, y, z)
+
+    P = morton_partition(world)
+    n_glob = tuple(args.grid * p for p in P) if args.scaling == "weak" else (args.grid,) * 3
+
+    if args.impl == "reference":
+        run_reference(args, n_glob, rank)
+        return
+
+    import numpy as np
+    import torch
+
+    import synth
+    import paper_2103_01597_b200 as b2
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = b2.MHD_F64 if args.dtype == "f64" else b2.MHD_F32
+    es = 8 if dtype == b2.MHD_F64 else 4
+    ds = synth.spacing(n_glob)
+    mesh = b2.Mesh(n_glob, ds, synth.P0, dtype, rank=rank, nranks=world, exchange_corners=args.corners,
+                   kernel=args.kernel)
+    nz, ny, nx = mesh.shape
+    lo = tuple(c * n for c, n in zip(reversed(mesh.coord), (nz, ny, nx)))
+    npdt = np.float64 if dtype == b2.MHD_F64 else np.float32
+    host = torch.from_numpy(synth.splitmix_state((n_glob[2], n_glob[1], n_glob[0]), lo, (nz, ny, nx),
+                                                 dtype=npdt)).pin_memory()
+    mesh.load(host)
+    dt = synth.DT
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        mesh.step(dt)
+    mesh.synchronize()
+
+    # ---- timed region: K full RK3 steps, device-timed on the mesh stream ----
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    l0 = mesh.launch_count()
+    mesh.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(mesh.stream)
+        for _ in range(args.steps):
+            mesh.step(dt)
+        ev1.record(mesh.stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = mesh.launch_count() - l0
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    prof = mesh.profile_read()
+    mesh.profile(False)
+    cells = n_glob[0] * n_glob[1] * n_glob[2]
+    value = cells * 3 * args.steps / (ms_total * 1e-3) / 1e9
+
+    # finiteness over the timed window: any NaN/Inf invalidates the run
+    finite = True
+    for q in range(8):
+        try:
+            mesh.reduce(q, b2.MHD_MAX)
+        except b2.MhdError:
+            finite = False
+
+    # ---- roofline of the dominant kernel (the fused update), from its live launch times ----
+    up = prof["update"]
+    upd_ms = up["ms"] / max(up["launches"], 1)
+    hbm_peak = peaks().get("hbm_gbs", 6650.0)
+    achieved_gbs = up["bytes"] / (up["ms"] * 1e-3) / 1e9 if up["ms"] > 0 else None
+    local_cells = nx * ny * nz
+    # FP64 lane operations per cell-substep of the canonical per-cell arithmetic
+    dp_per_cell = float(os.environ.get("B2_DP_PER_CELL", "0")) or None
+    substep_ms = ms_total / (3 * args.steps)
+    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved_gbs / hbm_peak if achieved_gbs else None, "traffic": None,
+                "kernel": "update (fused stencil + RHS + RK3)", "avg_launch_ms": upd_ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    step_share = up["ms"] / max(ms_total, 1e-9)
+    phases = {k: {"launches": v["launches"], "ms_per_substep": v["ms"] / (3 * args.steps)} for k, v in prof.items()}
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if args.e2e_steps > 0:
+        out_host = torch.empty_like(host).pin_memory()
+        mesh.load(host)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            mesh.load(host)          # H2D of the step's input state (pinned)
+            mesh.step(dt)
+            mesh.store(out=out_host)  # D2H of the step's result (blocking)
+        torch.cuda.synchronize()
+        el = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": cells * 3 * args.e2e_steps / el / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(host.numel() * es), "d2h_bytes_per_step": int(out_host.numel() * es)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(n_glob, ds, synth.P0, dt)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic",
+            "config": {"workload": (f"{n_glob[0]}^3" if len(set(n_glob)) == 1 else "x".join(map(str, n_glob)))
+                       + f" {args.dtype.upper()} MHD, 1 RK3 step (3 substeps) per bench step",
+                       "grid": list(n_glob), "local_grid": [nx, ny, nz], "partition": list(mesh.P),
+                       "substeps_per_step": 3, "dt": dt, "params": "P0",
+                       "l2": "inputs larger than L2 (no flush)", "kernel": args.kernel,
+                       "exchange_corners": bool(args.corners)},
+            "ms_per_substep": substep_ms,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "roofline": roofline,
+            "update_share_of_step": step_share,
+            "phases": phases,
+            "finite": finite,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        if dp_per_cell:
+            ach = dp_per_cell * local_cells * (up["launches"] / max(up["launches"], 1)) / (upd_ms * 1e-3)
+            line["roofline_fp64"] = {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_LANE_OPS,
+                                     "unit": "DP lane-ops/s", "frac": ach / FP64_PEAK_LANE_OPS}
+        print(json.dumps(line), flush=True)
+    mesh.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

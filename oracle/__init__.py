@@ -91,13 +91,12 @@ def _params(p) -> Params:
 
 def set_threads(n: int) -> None:
     """OpenMP thread count for oracle_rhs (the only parallel loop; per-cell results do not depend on it)."""
-    os.environ["OMP_NUM_THREADS"] = str(n)
-    try:
-        import ctypes.util
-        gomp = ctypes.CDLL(ctypes.util.find_library("gomp") or "libgomp.so.1")
-        gomp.omp_set_num_threads(ctypes.c_int(n))
-    except OSError:
-        pass
+    for kind in LIB:
+        _lib(kind).oracle_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(_lib("d").oracle_get_threads())
 
 
 # --- grid helpers ------------------------------------------------------------------------------

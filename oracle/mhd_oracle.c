@@ -346,3 +346,13 @@ int oracle_rhs_of_state(real* const state[NF], int nx, int ny, int nz, const dou
 }
 
 int oracle_real_bytes(void) { return (int)sizeof(real); }
+
+/* OpenMP thread count of oracle_rhs (per-cell results do not depend on it). */
+#ifdef _OPENMP
+#include <omp.h>
+void oracle_set_threads(int n) { omp_set_num_threads(n); }
+int oracle_get_threads(void) { return omp_get_max_threads(); }
+#else
+void oracle_set_threads(int n) { (void)n; }
+int oracle_get_threads(void) { return 1; }
+#endif

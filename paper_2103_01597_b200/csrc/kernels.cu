@@ -1,0 +1,202 @@
+// Direct update kernel, halo segment copy/pack/unpack, load/store and reduction kernels.
+//
+// The direct kernel is one thread per cell, reading its 55-point neighbourhood
+// (Eq. 14) through the read-only data path.  It is the general-region
+// kernel (any box, used for the thin outer slabs of a decomposed subdomain)
+// and the correctness baseline of the z-marching kernel; both run the canonical
+// per-cell arithmetic of mhd_math.cuh.
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace b2 {
+
+template <typename T>
+struct GAcc {
+  Fields<T> F;
+  long long base, sy, sz;
+  __device__ __forceinline__ T operator()(int q, int dx, int dy, int dz) const {
+    return __ldg(F.f[q] + base + (long long)dz * sz + (long long)dy * sy + dx);
+  }
+};
+
+// MODE 0: RK3 update into `out` (which holds f_{k-1} for k > 0); MODE 1: RHS to rhs_out.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out, Geom g, Region r, Coef<T> C,
+                                                     int k, T* __restrict__ rhs_out) {
+  const int x = r.lo[0] + blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = r.lo[1] + blockIdx.y * blockDim.y + threadIdx.y;
+  const int z = r.lo[2] + blockIdx.z * blockDim.z + threadIdx.z;
+  if (x >= r.lo[0] + r.ext[0] || y >= r.lo[1] + r.ext[1] || z >= r.lo[2] + r.ext[2]) return;
+  const long long base = (long long)z * g.sz + (long long)y * g.sy + x;
+  GAcc<T> V{in, base, g.sy, g.sz};
+  Derivs<T> D;
+  gather<T>(V, C, D);
+  T rhs[NF];
+  rhs_cell<T>(D, C, rhs);
+  if (MODE == 0) {
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      const T fprev = k > 0 ? out.f[q][base] : (T)0;
+      out.f[q][base] = rk_update<T>(k, D.f[q], fprev, rhs[q], C);
+    }
+  } else {
+    const long long n = (long long)g.nx * g.ny * g.nz;
+    const long long li = ((long long)z * g.ny + y) * g.nx + x;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) rhs_out[q * n + li] = rhs[q];
+  }
+}
+
+template <typename T>
+void launch_direct(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, const Geom& g, const Region& r,
+                   const Coef<T>& C, int k, T* rhs_out) {
+  if (r.ext[0] <= 0 || r.ext[1] <= 0 || r.ext[2] <= 0) return;
+  // thin x-slabs of the outer shell get a block shaped along y
+  const dim3 blk = r.ext[0] >= 16 ? dim3(32, 4, 1) : dim3(r.ext[0], (128 / r.ext[0]) < 32 ? (128 / r.ext[0]) : 32, 1);
+  dim3 grd((r.ext[0] + blk.x - 1) / blk.x, (r.ext[1] + blk.y - 1) / blk.y, (r.ext[2] + blk.z - 1) / blk.z);
+  if (rhs_out)
+    direct_kernel<T, 1><<<grd, blk, 0, st>>>(in, out, g, r, C, k, rhs_out);
+  else
+    direct_kernel<T, 0><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr);
+}
+
+// ---- halo segments ---------------------------------------------------------
+// One launch covers every segment of a list; each block belongs to exactly one segment.
+template <typename T, int KIND>
+__global__ void __launch_bounds__(256) seg_kernel(Fields<T> F, Geom g, SegList L, T* __restrict__ buf) {
+  int s = 0;
+  while (s + 1 < L.n && (int)blockIdx.x >= L.s[s + 1].block0) ++s;
+  const SegDesc& d = L.s[s];
+  const long long c = (long long)(blockIdx.x - d.block0) * blockDim.x + threadIdx.x;
+  if (c >= d.count) return;
+  const int cx = (int)(c % d.ext[0]);
+  const long long rr = c / d.ext[0];
+  const int cy = (int)(rr % d.ext[1]);
+  const int cz = (int)(rr / d.ext[1]);
+  const long long so = (long long)(d.src[2] + cz) * g.sz + (long long)(d.src[1] + cy) * g.sy + (d.src[0] + cx);
+  const long long dof = (long long)(d.dst[2] + cz) * g.sz + (long long)(d.dst[1] + cy) * g.sy + (d.dst[0] + cx);
+#pragma unroll
+  for (int q = 0; q < NF; ++q) {
+    if (KIND == SEG_SELF) F.f[q][dof] = F.f[q][so];
+    if (KIND == SEG_PACK) buf[d.buf_off + q * d.count + c] = F.f[q][so];
+    if (KIND == SEG_UNPACK) F.f[q][dof] = buf[d.buf_off + q * d.count + c];
+  }
+}
+
+template <typename T>
+void launch_segments(cudaStream_t st, const Fields<T>& fl, const Geom& g, const SegList& L, int kind, T* buf) {
+  if (L.n == 0 || L.nblocks == 0) return;
+  if (kind == SEG_SELF) seg_kernel<T, SEG_SELF><<<L.nblocks, 256, 0, st>>>(fl, g, L, buf);
+  if (kind == SEG_PACK) seg_kernel<T, SEG_PACK><<<L.nblocks, 256, 0, st>>>(fl, g, L, buf);
+  if (kind == SEG_UNPACK) seg_kernel<T, SEG_UNPACK><<<L.nblocks, 256, 0, st>>>(fl, g, L, buf);
+}
+
+// ---- load / store: contiguous local interior <-> pitched field ----------------------------------
+template <typename TS, typename TD>
+__global__ void copy_in_kernel(const TS* __restrict__ src, TD* origin, Geom g) {
+  const long long n = (long long)g.nx * g.ny * g.nz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % g.nx);
+    const long long r = i / g.nx;
+    const int y = (int)(r % g.ny);
+    const int z = (int)(r / g.ny);
+    origin[(long long)z * g.sz + (long long)y * g.sy + x] = (TD)src[i];
+  }
+}
+template <typename TS, typename TD>
+__global__ void copy_out_kernel(const TS* origin, TD* __restrict__ dst, Geom g) {
+  const long long n = (long long)g.nx * g.ny * g.nz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % g.nx);
+    const long long r = i / g.nx;
+    const int y = (int)(r % g.ny);
+    const int z = (int)(r / g.ny);
+    dst[i] = (TD)origin[(long long)z * g.sz + (long long)y * g.sy + x];
+  }
+}
+template <typename TS, typename TD>
+void launch_copy_in(cudaStream_t st, const TS* src, TD* origin, const Geom& g) {
+  copy_in_kernel<TS, TD><<<148 * 8, 256, 0, st>>>(src, origin, g);
+}
+template <typename TS, typename TD>
+void launch_copy_out(cudaStream_t st, const TS* origin, TD* dst, const Geom& g) {
+  copy_out_kernel<TS, TD><<<148 * 8, 256, 0, st>>>(origin, dst, g);
+}
+
+// ---- reductions (min, max, sum, sum of squares, sum of exp), two stages ----------------------------
+__device__ __forceinline__ void red_combine(double* a, const double* b) {
+  a[0] = fmin(a[0], b[0]);
+  a[1] = fmax(a[1], b[1]);
+  a[2] += b[2];
+  a[3] += b[3];
+  a[4] += b[4];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_stage1(const T* origin, Geom g, double* partial) {
+  double v[kReduceVals] = {DBL_MAX, -DBL_MAX, 0.0, 0.0, 0.0};
+  const long long n = (long long)g.nx * g.ny * g.nz;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % g.nx);
+    const long long r = i / g.nx;
+    const int y = (int)(r % g.ny);
+    const int z = (int)(r / g.ny);
+    const double f = (double)origin[(long long)z * g.sz + (long long)y * g.sy + x];
+    // NaN propagates through fmin/fmax only if both are NaN: track it in the sum instead
+    v[0] = fmin(v[0], f);
+    v[1] = fmax(v[1], f);
+    v[2] += f;
+    v[3] += f * f;
+    v[4] += exp(f);
+  }
+  __shared__ double sh[256][kReduceVals];
+  for (int j = 0; j < kReduceVals; ++j) sh[threadIdx.x][j] = v[j];
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red_combine(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int j = 0; j < kReduceVals; ++j) partial[blockIdx.x * kReduceVals + j] = sh[0][j];
+}
+
+__global__ void reduce_stage2(double* partial, int nblocks) {
+  __shared__ double sh[256][kReduceVals];
+  double v[kReduceVals] = {DBL_MAX, -DBL_MAX, 0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) red_combine(v, partial + b * kReduceVals);
+  for (int j = 0; j < kReduceVals; ++j) sh[threadIdx.x][j] = v[j];
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red_combine(sh[threadIdx.x], sh[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int j = 0; j < kReduceVals; ++j) partial[j] = sh[0][j];
+}
+
+template <typename T>
+void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scratch, int nblocks) {
+  reduce_stage1<T><<<nblocks, 256, 0, st>>>(origin, g, scratch);
+  reduce_stage2<<<1, 256, 0, st>>>(scratch, nblocks);
+}
+
+// ---- explicit instantiations ----------------------------------------------------------------------
+#define B2_INST(T)                                                                                       \
+  template void launch_direct<T>(cudaStream_t, const Fields<T>&, const Fields<T>&, const Geom&,           \
+                                 const Region&, const Coef<T>&, int, T*);                                 \
+  template void launch_segments<T>(cudaStream_t, const Fields<T>&, const Geom&, const SegList&, int, T*); \
+  template void launch_reduce<T>(cudaStream_t, const T*, const Geom&, double*, int);
+B2_INST(float)
+B2_INST(double)
+#undef B2_INST
+template void launch_copy_in<float, float>(cudaStream_t, const float*, float*, const Geom&);
+template void launch_copy_in<double, double>(cudaStream_t, const double*, double*, const Geom&);
+template void launch_copy_in<float, double>(cudaStream_t, const float*, double*, const Geom&);
+template void launch_copy_in<double, float>(cudaStream_t, const double*, float*, const Geom&);
+template void launch_copy_out<float, float>(cudaStream_t, const float*, float*, const Geom&);
+template void launch_copy_out<double, double>(cudaStream_t, const double*, double*, const Geom&);
+template void launch_copy_out<float, double>(cudaStream_t, const float*, double*, const Geom&);
+template void launch_copy_out<double, float>(cudaStream_t, const double*, float*, const Geom&);
+
+}  // namespace b2

@@ -1,0 +1,850 @@
+// Host runtime and C ABI of b2mhd (include/b2mhd.h).
+//
+//  * decomposition: Morton mapping P:557 (Z-order, rank -> subdomain), n' = n / p
+//  * halo segments: 6 sides, 12 edges, 8 corners; segments to one peer are
+//    concatenated in canonical order, so one NCCL send/recv pair per distinct peer
+//    replaces the paper's per-segment MPI_Isend/Irecv with tags
+//  * the ISL iteration pipeline: pack on a high-priority comm stream, NCCL
+//    exchange there, the inner-segment update concurrently on the compute stream, then
+//    unpack -> event -> outer segments.  Stream order replaces the paper's per-iteration
+//    cudaDeviceSynchronize + MPI_Barrier.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/b2mhd.h"
+#include "kernels.h"
+
+using namespace b2;
+
+namespace {
+
+thread_local std::string g_err;
+
+mhd_status fail(mhd_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CU(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(MHD_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+#define NC(call)                                                                                   \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess) return fail(MHD_ENCCL, std::string(#call ": ") + ncclGetErrorString(r_)); \
+  } while (0)
+
+// ---- Morton mapping: bit 3k + j of the index is bit k of coordinate j ----------------
+void morton_decode(uint32_t idx, int c[3]) {
+  c[0] = c[1] = c[2] = 0;
+  for (int k = 0; k < 10; ++k)
+    for (int j = 0; j < 3; ++j) c[j] |= (int)(((idx >> (3 * k + j)) & 1u) << k);
+}
+uint32_t morton_encode(const int c[3]) {
+  uint32_t idx = 0;
+  for (int k = 0; k < 10; ++k)
+    for (int j = 0; j < 3; ++j) idx |= (uint32_t)((c[j] >> k) & 1) << (3 * k + j);
+  return idx;
+}
+// Morton coordinate j maps to memory axis (2 - j): coordinate 0 -> z (reading R#16).
+void partition_xyz(int nranks, int P[3]) {
+  int m[3];
+  morton_decode((uint32_t)(nranks - 1), m);
+  for (int j = 0; j < 3; ++j) P[2 - j] = m[j] + 1;
+}
+void coord_xyz(int rank, int c[3]) {
+  int m[3];
+  morton_decode((uint32_t)rank, m);
+  for (int j = 0; j < 3; ++j) c[2 - j] = m[j];
+}
+int rank_of_xyz(const int c[3]) {
+  int m[3] = {c[2], c[1], c[0]};
+  return (int)morton_encode(m);
+}
+
+mhd_status check_info(const mhd_mesh_info* info) {
+  if (!info) return fail(MHD_EINVAL, "info is null");
+  if (info->abi_version != MHD_ABI_VERSION) return fail(MHD_EUNSUPPORTED, "ABI version mismatch");
+  if (info->radius != MHD_RADIUS) return fail(MHD_EUNSUPPORTED, "only radius 3 (6th order) is built");
+  if (info->dtype != MHD_F32 && info->dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "dtype must be F32 or F64");
+  if (info->nranks < 1 || (info->nranks & (info->nranks - 1)) != 0)
+    return fail(MHD_EDECOMP, "nranks must be a power of two (Morton partition, P:557)");
+  if (info->rank < 0 || info->rank >= info->nranks) return fail(MHD_EINVAL, "rank out of range");
+  for (int a = 0; a < 3; ++a) {
+    if (info->n[a] < 1) return fail(MHD_EINVAL, "n must be positive");
+    if (!(info->ds[a] > 0)) return fail(MHD_EINVAL, "ds must be positive");
+  }
+  int P[3];
+  partition_xyz(info->nranks, P);
+  for (int a = 0; a < 3; ++a) {
+    if (info->n[a] % P[a] != 0) return fail(MHD_EDECOMP, "p_i does not divide n_i (P:207)");
+    if (info->n[a] / P[a] <= 2 * MHD_RADIUS) return fail(MHD_ESMALL, "local extent n'_i <= 2r (P:705)");
+  }
+  return MHD_OK;
+}
+
+struct SegInfo {
+  mhd_segment s;
+  bool self;
+};
+
+// Segments of one rank in canonical order: sides, edges, corners; lexicographic (oz, oy, ox).
+std::vector<SegInfo> build_segments(const mhd_mesh_info* info, int rank) {
+  int P[3], c[3];
+  partition_xyz(info->nranks, P);
+  coord_xyz(rank, c);
+  int64_t n[3];
+  for (int a = 0; a < 3; ++a) n[a] = info->n[a] / P[a];
+  std::vector<SegInfo> out;
+  for (int kind = 1; kind <= 3; ++kind) {
+    if (kind == 3 && !info->exchange_corners) continue;
+    for (int oz = -1; oz <= 1; ++oz)
+      for (int oy = -1; oy <= 1; ++oy)
+        for (int ox = -1; ox <= 1; ++ox) {
+          const int o[3] = {ox, oy, oz};
+          if ((ox != 0) + (oy != 0) + (oz != 0) != kind) continue;
+          SegInfo si;
+          memset(&si, 0, sizeof(si));
+          mhd_segment& s = si.s;
+          s.kind = kind;
+          int rc[3], sc[3];
+          for (int a = 0; a < 3; ++a) {
+            s.offset[a] = o[a];
+            // halo cells at offset o (receiver side) and the interior cells that fill them
+            // (sender side): s' = ((s - r) mod n') + r, in interior coordinates
+            s.dst_first[a] = o[a] < 0 ? -MHD_RADIUS : (o[a] == 0 ? 0 : (int)n[a]);
+            s.src_first[a] = o[a] < 0 ? (int)n[a] - MHD_RADIUS : 0;
+            s.extent[a] = o[a] == 0 ? (int)n[a] : MHD_RADIUS;
+            rc[a] = ((c[a] + o[a]) % P[a] + P[a]) % P[a];
+            sc[a] = ((c[a] - o[a]) % P[a] + P[a]) % P[a];
+          }
+          s.recv_peer = rank_of_xyz(rc);
+          s.send_peer = rank_of_xyz(sc);
+          si.self = s.recv_peer == rank;  // then also send_peer == rank
+          s.send_buf_cell = s.recv_buf_cell = -1;
+          out.push_back(si);
+        }
+  }
+  // buffer offsets: per peer, concatenation in canonical order
+  std::vector<int64_t> sc(info->nranks, 0), rcnt(info->nranks, 0);
+  for (auto& si : out) {
+    if (si.self) continue;
+    const int64_t cells = (int64_t)si.s.extent[0] * si.s.extent[1] * si.s.extent[2];
+    si.s.send_buf_cell = sc[si.s.send_peer];
+    sc[si.s.send_peer] += cells;
+    si.s.recv_buf_cell = rcnt[si.s.recv_peer];
+    rcnt[si.s.recv_peer] += cells;
+  }
+  return out;
+}
+
+template <typename T>
+Coef<T> make_coef(const mhd_mesh_info& info, int k, double dt) {
+  Coef<T> C;
+  const double c[3] = {3.0 / 4.0, -3.0 / 20.0, 1.0 / 60.0};
+  const double d[3] = {3.0 / 2.0, -3.0 / 20.0, 1.0 / 90.0};
+  const double c0 = -49.0 / 18.0;
+  const double e[3] = {270.0 / 720.0, -27.0 / 720.0, 2.0 / 720.0};
+  const double* ds = info.ds;
+  for (int a = 0; a < 3; ++a) {
+    for (int i = 0; i < 3; ++i) {
+      C.c1[a][i] = (T)(c[i] / ds[a]);
+      C.d2[a][i] = (T)(d[i] / (ds[a] * ds[a]));
+    }
+    C.d0[a] = (T)(c0 / (ds[a] * ds[a]));
+  }
+  const int pa[3] = {0, 0, 1}, pb[3] = {1, 2, 2};
+  for (int p = 0; p < 3; ++p)
+    for (int i = 0; i < 3; ++i) C.xw[p][i] = (T)(e[i] / (ds[pa[p]] * ds[pb[p]]));
+  const mhd_params& ph = info.phys;
+  C.gamma_cp = (T)(ph.gamma / ph.cp);
+  C.gm1 = (T)(ph.gamma - 1.0);
+  C.inv_cp = (T)(1.0 / ph.cp);
+  C.lnrho0 = (T)ph.lnrho0;
+  C.cs0sq = (T)(ph.cs0 * ph.cs0);
+  C.inv_T0 = (T)std::exp(-ph.lnT0);
+  C.H_C = (T)(ph.H - ph.C);
+  C.eta_inv_mu0 = (T)(ph.eta / ph.mu0);
+  C.inv_mu0 = (T)(1.0 / ph.mu0);
+  C.nu = (T)ph.nu;
+  C.nu3 = (T)(ph.nu / 3.0);
+  C.two_nu = (T)(2.0 * ph.nu);
+  C.zeta = (T)ph.zeta;
+  C.eta = (T)ph.eta;
+  C.K = (T)ph.K;
+  // Williamson (1980) 2N RK3 (R#3)
+  const double alpha[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
+  const double beta[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+  for (int j = 0; j < 3; ++j) {
+    C.rkB[j] = (T)(beta[j] * dt);
+    C.rkA[j] = j == 0 ? (T)0 : (T)(beta[j] * alpha[j] / beta[j - 1]);
+  }
+  (void)k;
+  return C;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+  int64_t n[3];
+  int64_t xo;    // elements of left pad: interior x = 0 sits at row offset xo (128-byte aligned)
+  int64_t sy, sz, field_elems, origin;
+  size_t field_bytes, state_off[2], send_off, recv_off, red_off, total;
+  int64_t send_cells, recv_cells;
+};
+
+Layout make_layout(const mhd_mesh_info* info, int rank, const std::vector<SegInfo>& segs) {
+  Layout L;
+  int P[3];
+  partition_xyz(info->nranks, P);
+  const size_t es = (size_t)info->dtype;
+  const int64_t al = 128 / (int64_t)es;
+  for (int a = 0; a < 3; ++a) L.n[a] = info->n[a] / P[a];
+  L.xo = al;
+  L.sy = (int64_t)align_up((size_t)(L.xo + L.n[0] + MHD_RADIUS + 1), (size_t)al);
+  L.sz = L.sy * (L.n[1] + 2 * MHD_RADIUS);
+  L.field_elems = (int64_t)align_up((size_t)(L.sz * (L.n[2] + 2 * MHD_RADIUS) + 2 * al), (size_t)(256 / es));
+  L.origin = MHD_RADIUS * L.sz + MHD_RADIUS * L.sy + L.xo;
+  L.field_bytes = (size_t)L.field_elems * es;
+  size_t off = 0;
+  for (int s = 0; s < 2; ++s) {
+    L.state_off[s] = off;
+    off += NF * L.field_bytes;
+  }
+  L.send_cells = L.recv_cells = 0;
+  for (auto& si : segs)
+    if (!si.self) {
+      const int64_t cells = (int64_t)si.s.extent[0] * si.s.extent[1] * si.s.extent[2];
+      L.send_cells += cells;
+      L.recv_cells += cells;
+    }
+  (void)rank;
+  L.send_off = off;
+  off = align_up(off + (size_t)L.send_cells * NF * es, 256);
+  L.recv_off = off;
+  off = align_up(off + (size_t)L.recv_cells * NF * es, 256);
+  L.red_off = off;
+  off = align_up(off + kReduceBlocks * kReduceVals * sizeof(double), 256);
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+struct PeerXfer {
+  int peer;
+  int64_t send_cell0, send_cells, recv_cell0, recv_cells;
+};
+
+struct mhd_mesh {
+  mhd_mesh_info info;
+  int P[3], coord[3];
+  Layout L;
+  Geom g;
+  char* ws;
+  cudaStream_t stream;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  std::vector<SegInfo> segs;
+  std::vector<PeerXfer> peers;
+  SegList self_list, pack_list, unpack_list;
+  ncclComm_t comm = nullptr;
+  int cur = 0;
+  int next_k = 0;
+  int variant = 0;
+  int64_t launches = 0;
+  double* h_red = nullptr;  // pinned
+  // profiling: (start, stop) event pairs per phase, with the algorithmic bytes of the launch
+  struct Rec {
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  bool prof = false;
+  std::vector<Rec> recs[MHD_NPHASES];
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take_event() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+
+  template <typename T>
+  Fields<T> fields(int s) const {
+    Fields<T> F;
+    for (int q = 0; q < NF; ++q)
+      F.f[q] = reinterpret_cast<T*>(ws + L.state_off[s] + (size_t)q * L.field_bytes) + L.origin;
+    return F;
+  }
+  template <typename T>
+  T* send_buf() const { return reinterpret_cast<T*>(ws + L.send_off); }
+  template <typename T>
+  T* recv_buf() const { return reinterpret_cast<T*>(ws + L.recv_off); }
+  double* red_scratch() const { return reinterpret_cast<double*>(ws + L.red_off); }
+  bool distributed() const { return info.nranks > 1; }
+};
+
+namespace {
+
+SegList make_list(const mhd_mesh& m, bool self, bool send) {
+  SegList Ls;
+  memset(&Ls, 0, sizeof(Ls));
+  int nb = 0;
+  for (auto& si : m.segs) {
+    if (si.self != self) continue;
+    SegDesc& d = Ls.s[Ls.n++];
+    for (int a = 0; a < 3; ++a) {
+      d.src[a] = si.s.src_first[a];
+      d.dst[a] = si.s.dst_first[a];
+      d.ext[a] = si.s.extent[a];
+    }
+    d.count = (long long)d.ext[0] * d.ext[1] * d.ext[2];
+    d.buf_off = 0;
+    if (!self) {
+      // global buffer offset = peer base + cell offset inside the peer's buffer, in values
+      for (auto& p : m.peers) {
+        if (send && p.peer == si.s.send_peer) d.buf_off = (p.send_cell0 + si.s.send_buf_cell) * NF;
+        if (!send && p.peer == si.s.recv_peer) d.buf_off = (p.recv_cell0 + si.s.recv_buf_cell) * NF;
+      }
+    }
+    d.block0 = nb;
+    nb += (int)((d.count + 255) / 256);
+  }
+  Ls.nblocks = nb;
+  return Ls;
+}
+
+// Phase timer: records a start event now and the stop event when it goes out of scope.
+struct PhaseTimer {
+  mhd_mesh* m;
+  cudaStream_t st;
+  int phase;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  PhaseTimer(mhd_mesh* m_, cudaStream_t s_, int ph, double by) : m(m_), st(s_), phase(ph), bytes(by) {
+    if (m->prof) {
+      a = m->take_event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~PhaseTimer() {
+    if (!a) return;
+    cudaEvent_t b = m->take_event();
+    cudaEventRecord(b, st);
+    m->recs[phase].push_back({a, b, bytes});
+  }
+};
+
+double seg_bytes(const SegList& L, size_t es) {
+  double c = 0;
+  for (int i = 0; i < L.n; ++i) c += (double)L.s[i].count;
+  return c * NF * (double)es * 2.0;
+}
+
+// The update of one region of the subdomain.
+template <typename T>
+void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out) {
+  const Fields<T> in = m->fields<T>(m->cur), out = m->fields<T>(1 - m->cur);
+  const Coef<T> C = make_coef<T>(m->info, k, dt);
+  const bool zm = m->variant != 1 && zmarch_supported<T>(m->g, r);
+  const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
+  PhaseTimer t(m, m->stream, MHD_PHASE_UPDATE, cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
+  if (zm)
+    launch_zmarch<T>(m->stream, in, out, m->g, r, C, k, rhs_out);
+  else
+    launch_direct<T>(m->stream, in, out, m->g, r, C, k, rhs_out);
+  m->launches++;
+}
+
+template <typename T>
+mhd_status halo_begin(mhd_mesh* m) {
+  const Fields<T> F = m->fields<T>(m->cur);
+  if (m->self_list.n) {
+    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
+    launch_segments<T>(m->stream, F, m->g, m->self_list, SEG_SELF, nullptr);
+    m->launches++;
+  }
+  if (!m->distributed() || m->peers.empty()) return MHD_OK;
+  if (!m->comm) return fail(MHD_ENCCL, "mhd_comm_init was not called");
+  CU(cudaEventRecord(m->ev_ready, m->stream));
+  CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
+  {
+    PhaseTimer t(m, m->comm_stream, MHD_PHASE_PACK, seg_bytes(m->pack_list, sizeof(T)));
+    launch_segments<T>(m->comm_stream, F, m->g, m->pack_list, SEG_PACK, m->send_buf<T>());
+    m->launches++;
+  }
+  {
+    const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+    PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, seg_bytes(m->pack_list, sizeof(T)));
+    NC(ncclGroupStart());
+    for (auto& p : m->peers) {
+      NC(ncclSend(m->send_buf<T>() + p.send_cell0 * NF, (size_t)p.send_cells * NF, dt, p.peer, m->comm, m->comm_stream));
+      NC(ncclRecv(m->recv_buf<T>() + p.recv_cell0 * NF, (size_t)p.recv_cells * NF, dt, p.peer, m->comm, m->comm_stream));
+    }
+    NC(ncclGroupEnd());
+  }
+  {
+    PhaseTimer t(m, m->comm_stream, MHD_PHASE_UNPACK, seg_bytes(m->unpack_list, sizeof(T)));
+    launch_segments<T>(m->comm_stream, F, m->g, m->unpack_list, SEG_UNPACK, m->recv_buf<T>());
+    m->launches++;
+  }
+  CU(cudaEventRecord(m->ev_halo, m->comm_stream));
+  return MHD_OK;
+}
+
+template <typename T>
+mhd_status halo_end(mhd_mesh* m) {
+  if (m->distributed() && !m->peers.empty()) CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
+  return MHD_OK;
+}
+
+// Inner region and outer slabs: only axes split across ranks need the
+// remote halo; along unsplit axes the whole extent is inner (its halo is a self copy).
+void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer) {
+  const int n[3] = {m->g.nx, m->g.ny, m->g.nz};
+  bool split[3];
+  for (int a = 0; a < 3; ++a) {
+    split[a] = m->P[a] > 1;
+    inner.lo[a] = split[a] ? MHD_RADIUS : 0;
+    inner.ext[a] = split[a] ? n[a] - 2 * MHD_RADIUS : n[a];
+  }
+  outer.clear();
+  // slabs: z first (full x, y), then y (full x, inner z), then x (inner y, z)
+  int lo[3] = {0, 0, 0}, hi[3] = {n[0], n[1], n[2]};
+  for (int a = 2; a >= 0; --a) {
+    if (!split[a]) continue;
+    for (int side = 0; side < 2; ++side) {
+      Region r;
+      for (int b = 0; b < 3; ++b) {
+        r.lo[b] = lo[b];
+        r.ext[b] = hi[b] - lo[b];
+      }
+      r.lo[a] = side == 0 ? 0 : n[a] - MHD_RADIUS;
+      r.ext[a] = MHD_RADIUS;
+      outer.push_back(r);
+    }
+    lo[a] = MHD_RADIUS;
+    hi[a] = n[a] - MHD_RADIUS;
+  }
+}
+
+template <typename T>
+mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
+  mhd_status st = halo_begin<T>(m);
+  if (st != MHD_OK) return st;
+  Region inner;
+  std::vector<Region> outer;
+  split_regions(m, inner, outer);
+  update_region<T>(m, inner, k, dt, rhs_out);
+  st = halo_end<T>(m);
+  if (st != MHD_OK) return st;
+  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out);
+  CU(cudaGetLastError());
+  return MHD_OK;
+}
+
+}  // namespace
+
+namespace {
+template <typename TM>
+mhd_status load_impl(mhd_mesh* m, int field, const void* src, int src_dtype, int on_device) {
+  TM* origin = m->fields<TM>(m->cur).f[field];
+  const size_t es = (size_t)src_dtype;
+  const size_t ncell = (size_t)m->g.nx * m->g.ny * m->g.nz;
+  if (src_dtype == (int)sizeof(TM)) {
+    cudaMemcpy3DParms p;
+    memset(&p, 0, sizeof(p));
+    p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), (size_t)m->g.nx * es, (size_t)m->g.nx, (size_t)m->g.ny);
+    p.dstPtr = make_cudaPitchedPtr(origin, (size_t)m->g.sy * es, (size_t)m->g.sy, (size_t)(m->g.ny + 2 * MHD_RADIUS));
+    p.extent = make_cudaExtent((size_t)m->g.nx * es, (size_t)m->g.ny, (size_t)m->g.nz);
+    p.kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CU(cudaMemcpy3DAsync(&p, m->stream));
+    return MHD_OK;
+  }
+  const void* dsrc = src;
+  void* tmp = nullptr;
+  if (!on_device) {
+    CU(cudaMallocAsync(&tmp, ncell * es, m->stream));
+    CU(cudaMemcpyAsync(tmp, src, ncell * es, cudaMemcpyHostToDevice, m->stream));
+    dsrc = tmp;
+  }
+  if (src_dtype == MHD_F32)
+    launch_copy_in<float, TM>(m->stream, static_cast<const float*>(dsrc), origin, m->g);
+  else
+    launch_copy_in<double, TM>(m->stream, static_cast<const double*>(dsrc), origin, m->g);
+  m->launches++;
+  if (tmp) CU(cudaFreeAsync(tmp, m->stream));
+  return MHD_OK;
+}
+
+template <typename TM>
+mhd_status store_impl(mhd_mesh* m, int field, void* dst, int dst_dtype, int on_device) {
+  const TM* origin = m->fields<TM>(m->cur).f[field];
+  const size_t es = (size_t)dst_dtype;
+  const size_t ncell = (size_t)m->g.nx * m->g.ny * m->g.nz;
+  if (dst_dtype == (int)sizeof(TM)) {
+    cudaMemcpy3DParms p;
+    memset(&p, 0, sizeof(p));
+    p.srcPtr = make_cudaPitchedPtr(const_cast<TM*>(origin), (size_t)m->g.sy * es, (size_t)m->g.sy,
+                                   (size_t)(m->g.ny + 2 * MHD_RADIUS));
+    p.dstPtr = make_cudaPitchedPtr(dst, (size_t)m->g.nx * es, (size_t)m->g.nx, (size_t)m->g.ny);
+    p.extent = make_cudaExtent((size_t)m->g.nx * es, (size_t)m->g.ny, (size_t)m->g.nz);
+    p.kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CU(cudaMemcpy3DAsync(&p, m->stream));
+  } else {
+    void* tmp = nullptr;
+    void* ddst = dst;
+    if (!on_device) {
+      CU(cudaMallocAsync(&tmp, ncell * es, m->stream));
+      ddst = tmp;
+    }
+    if (dst_dtype == MHD_F32)
+      launch_copy_out<TM, float>(m->stream, origin, static_cast<float*>(ddst), m->g);
+    else
+      launch_copy_out<TM, double>(m->stream, origin, static_cast<double*>(ddst), m->g);
+    m->launches++;
+    if (tmp) {
+      CU(cudaMemcpyAsync(dst, tmp, ncell * es, cudaMemcpyDeviceToHost, m->stream));
+      CU(cudaFreeAsync(tmp, m->stream));
+    }
+  }
+  if (!on_device) CU(cudaStreamSynchronize(m->stream));
+  return MHD_OK;
+}
+}  // namespace
+
+// =================================================================================================
+extern "C" {
+
+const char* mhd_status_str(mhd_status s) {
+  switch (s) {
+    case MHD_OK: return "ok";
+    case MHD_EINVAL: return "invalid argument";
+    case MHD_EDECOMP: return "invalid decomposition";
+    case MHD_ESMALL: return "subdomain too small";
+    case MHD_EUNSUPPORTED: return "unsupported";
+    case MHD_ECUDA: return "CUDA error";
+    case MHD_ENCCL: return "NCCL error";
+    case MHD_ENOMEM: return "workspace too small";
+    case MHD_ENONFINITE: return "non-finite value";
+    case MHD_ESTATE: return "substep out of order";
+  }
+  return "unknown status";
+}
+
+const char* mhd_last_error(void) { return g_err.c_str(); }
+int32_t mhd_abi_version(void) { return MHD_ABI_VERSION; }
+
+mhd_status mhd_decompose(const mhd_mesh_info* info, int32_t rank, int32_t P[3], int32_t coord[3],
+                         int64_t local_n[3]) {
+  mhd_mesh_info tmp;
+  if (!info) return fail(MHD_EINVAL, "info is null");
+  tmp = *info;
+  tmp.rank = rank;
+  mhd_status st = check_info(&tmp);
+  if (st != MHD_OK) return st;
+  int p[3], c[3];
+  partition_xyz(info->nranks, p);
+  coord_xyz(rank, c);
+  for (int a = 0; a < 3; ++a) {
+    if (P) P[a] = p[a];
+    if (coord) coord[a] = c[a];
+    if (local_n) local_n[a] = info->n[a] / p[a];
+  }
+  return MHD_OK;
+}
+
+mhd_status mhd_segment_table(const mhd_mesh_info* info, int32_t rank, mhd_segment* out, int32_t max_segments,
+                             int32_t* count) {
+  mhd_mesh_info tmp;
+  if (!info || !count) return fail(MHD_EINVAL, "null argument");
+  tmp = *info;
+  tmp.rank = rank;
+  mhd_status st = check_info(&tmp);
+  if (st != MHD_OK) return st;
+  auto segs = build_segments(&tmp, rank);
+  *count = (int32_t)segs.size();
+  for (int i = 0; i < (int)segs.size() && i < max_segments; ++i) out[i] = segs[i].s;
+  return MHD_OK;
+}
+
+mhd_status mhd_workspace_bytes(const mhd_mesh_info* info, size_t* bytes) {
+  mhd_status st = check_info(info);
+  if (st != MHD_OK) return st;
+  if (!bytes) return fail(MHD_EINVAL, "bytes is null");
+  auto segs = build_segments(info, info->rank);
+  *bytes = make_layout(info, info->rank, segs).total;
+  return MHD_OK;
+}
+
+mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_t bytes, void* cuda_stream,
+                           mhd_mesh** out) {
+  mhd_status st = check_info(info);
+  if (st != MHD_OK) return st;
+  if (!dev_workspace || !out) return fail(MHD_EINVAL, "null workspace or out");
+  mhd_mesh* m = new mhd_mesh();
+  m->info = *info;
+  partition_xyz(info->nranks, m->P);
+  coord_xyz(info->rank, m->coord);
+  m->segs = build_segments(info, info->rank);
+  m->L = make_layout(info, info->rank, m->segs);
+  if (bytes < m->L.total) {
+    delete m;
+    return fail(MHD_ENOMEM, "workspace smaller than mhd_workspace_bytes");
+  }
+  m->g.nx = (int)m->L.n[0];
+  m->g.ny = (int)m->L.n[1];
+  m->g.nz = (int)m->L.n[2];
+  m->g.sy = m->L.sy;
+  m->g.sz = m->L.sz;
+  m->ws = static_cast<char*>(dev_workspace);
+  m->stream = static_cast<cudaStream_t>(cuda_stream);
+  // peers in rank order, each with a contiguous slice of the send and recv buffers
+  std::vector<int64_t> scount(info->nranks, 0), rcount(info->nranks, 0);
+  for (auto& si : m->segs)
+    if (!si.self) {
+      const int64_t cells = (int64_t)si.s.extent[0] * si.s.extent[1] * si.s.extent[2];
+      scount[si.s.send_peer] += cells;
+      rcount[si.s.recv_peer] += cells;
+    }
+  int64_t s0 = 0, r0 = 0;
+  for (int p = 0; p < info->nranks; ++p) {
+    if (scount[p] == 0 && rcount[p] == 0) continue;
+    m->peers.push_back(PeerXfer{p, s0, scount[p], r0, rcount[p]});
+    s0 += scount[p];
+    r0 += rcount[p];
+  }
+  m->self_list = make_list(*m, true, false);
+  m->pack_list = make_list(*m, false, true);
+  m->unpack_list = make_list(*m, false, false);
+  cudaError_t e = cudaMemsetAsync(m->ws, 0, m->L.total, m->stream);
+  if (e == cudaSuccess && info->nranks > 1) {
+    int lo, hi;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&m->comm_stream, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->ev_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->ev_halo, cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaMallocHost(&m->h_red, kReduceVals * sizeof(double));
+  if (e != cudaSuccess) {
+    delete m;
+    return fail(MHD_ECUDA, std::string("mesh create: ") + cudaGetErrorString(e));
+  }
+  *out = m;
+  return MHD_OK;
+}
+
+mhd_status mhd_nccl_unique_id(void* out128) {
+  if (!out128) return fail(MHD_EINVAL, "null out");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  memcpy(out128, &id, sizeof(id));
+  return MHD_OK;
+}
+
+mhd_status mhd_comm_init(mhd_mesh* m, const void* nccl_unique_id) {
+  if (!m || !nccl_unique_id) return fail(MHD_EINVAL, "null argument");
+  if (m->info.nranks == 1) return MHD_OK;
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof(id));
+  NC(ncclCommInitRank(&m->comm, m->info.nranks, id, m->info.rank));
+  return MHD_OK;
+}
+
+mhd_status mhd_mesh_destroy(mhd_mesh* m) {
+  if (!m) return MHD_OK;
+  cudaStreamSynchronize(m->stream);
+  if (m->comm) ncclCommDestroy(m->comm);
+  if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+  if (m->ev_ready) cudaEventDestroy(m->ev_ready);
+  if (m->ev_halo) cudaEventDestroy(m->ev_halo);
+  if (m->h_red) cudaFreeHost(m->h_red);
+  for (auto& v : m->recs)
+    for (auto& r : v) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  for (auto e : m->pool) cudaEventDestroy(e);
+  delete m;
+  return MHD_OK;
+}
+
+
+mhd_status mhd_load(mhd_mesh* m, int32_t field, const void* src, int32_t src_dtype, int32_t on_device) {
+  if (!m || !src || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad load argument");
+  if (src_dtype != MHD_F32 && src_dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "src dtype");
+  m->next_k = 0;
+  return m->info.dtype == MHD_F64 ? load_impl<double>(m, field, src, src_dtype, on_device)
+                                  : load_impl<float>(m, field, src, src_dtype, on_device);
+}
+
+mhd_status mhd_store(mhd_mesh* m, int32_t field, void* dst, int32_t dst_dtype, int32_t on_device) {
+  if (!m || !dst || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad store argument");
+  if (dst_dtype != MHD_F32 && dst_dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "dst dtype");
+  return m->info.dtype == MHD_F64 ? store_impl<double>(m, field, dst, dst_dtype, on_device)
+                                  : store_impl<float>(m, field, dst, dst_dtype, on_device);
+}
+
+mhd_status mhd_store_grid(mhd_mesh* m, int32_t field, void* dst, int32_t on_device) {
+  if (!m || !dst || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad store_grid argument");
+  const size_t es = (size_t)m->info.dtype;
+  const char* base = m->ws + m->L.state_off[m->cur] + (size_t)field * m->L.field_bytes;
+  const char* first = base + (size_t)(m->L.xo - MHD_RADIUS) * es;  // (x, y, z) = (-3, -3, -3)
+  const size_t mx = (size_t)m->g.nx + 2 * MHD_RADIUS, my = (size_t)m->g.ny + 2 * MHD_RADIUS;
+  const size_t mz = (size_t)m->g.nz + 2 * MHD_RADIUS;
+  CU(cudaMemcpy2DAsync(dst, mx * es, first, (size_t)m->g.sy * es, mx * es, my * mz,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, m->stream));
+  if (!on_device) CU(cudaStreamSynchronize(m->stream));
+  return MHD_OK;
+}
+
+mhd_status mhd_halo_exchange(mhd_mesh* m) {
+  if (!m) return fail(MHD_EINVAL, "null mesh");
+  mhd_status st = m->info.dtype == MHD_F64 ? halo_begin<double>(m) : halo_begin<float>(m);
+  if (st != MHD_OK) return st;
+  st = m->info.dtype == MHD_F64 ? halo_end<double>(m) : halo_end<float>(m);
+  if (st != MHD_OK) return st;
+  CU(cudaGetLastError());
+  return MHD_OK;
+}
+
+mhd_status mhd_integrate_substep(mhd_mesh* m, int32_t k, double dt) {
+  if (!m) return fail(MHD_EINVAL, "null mesh");
+  if (k < 0 || k > 2) return fail(MHD_EINVAL, "k must be 0, 1 or 2");
+  if (k != m->next_k) return fail(MHD_ESTATE, "substeps must run in the order 0, 1, 2");
+  mhd_status st = m->info.dtype == MHD_F64 ? substep_impl<double>(m, k, dt, nullptr)
+                                           : substep_impl<float>(m, k, dt, nullptr);
+  if (st != MHD_OK) return st;
+  m->cur = 1 - m->cur;
+  m->next_k = (k + 1) % 3;
+  return MHD_OK;
+}
+
+mhd_status mhd_integrate_step(mhd_mesh* m, double dt) {
+  for (int k = 0; k < 3; ++k) {
+    mhd_status st = mhd_integrate_substep(m, k, dt);
+    if (st != MHD_OK) return st;
+  }
+  return MHD_OK;
+}
+
+mhd_status mhd_debug_rhs(mhd_mesh* m, void* dev_dst) {
+  if (!m || !dev_dst) return fail(MHD_EINVAL, "null argument");
+  return m->info.dtype == MHD_F64 ? substep_impl<double>(m, 0, 0.0, static_cast<double*>(dev_dst))
+                                  : substep_impl<float>(m, 0, 0.0, static_cast<float*>(dev_dst));
+}
+
+mhd_status mhd_reduce(mhd_mesh* m, int32_t field, int32_t op, double* out) {
+  if (!m || !out || field < 0 || field >= NF || op < 0 || op > MHD_SUM_EXP) return fail(MHD_EINVAL, "bad reduce argument");
+  double* sc = m->red_scratch();
+  if (m->info.dtype == MHD_F64)
+    launch_reduce<double>(m->stream, m->fields<double>(m->cur).f[field], m->g, sc, kReduceBlocks);
+  else
+    launch_reduce<float>(m->stream, m->fields<float>(m->cur).f[field], m->g, sc, kReduceBlocks);
+  m->launches += 2;
+  if (m->distributed()) {
+    if (!m->comm) return fail(MHD_ENCCL, "mhd_comm_init was not called");
+    NC(ncclGroupStart());
+    NC(ncclAllReduce(sc + 0, sc + 0, 1, ncclFloat64, ncclMin, m->comm, m->stream));
+    NC(ncclAllReduce(sc + 1, sc + 1, 1, ncclFloat64, ncclMax, m->comm, m->stream));
+    NC(ncclAllReduce(sc + 2, sc + 2, 3, ncclFloat64, ncclSum, m->comm, m->stream));
+    NC(ncclGroupEnd());
+  }
+  CU(cudaMemcpyAsync(m->h_red, sc, kReduceVals * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  const double* v = m->h_red;
+  const double ncell = (double)m->info.n[0] * (double)m->info.n[1] * (double)m->info.n[2];
+  switch (op) {
+    case MHD_MIN: *out = v[0]; break;
+    case MHD_MAX: *out = v[1]; break;
+    case MHD_SUM: *out = v[2]; break;
+    case MHD_RMS: *out = std::sqrt(v[3] / ncell); break;
+    case MHD_SUM_EXP: *out = v[4]; break;
+  }
+  if (!std::isfinite(v[2]) || !std::isfinite(v[3]) || !std::isfinite(v[0]) || !std::isfinite(v[1]))
+    return fail(MHD_ENONFINITE, "field holds a NaN or Inf");
+  return MHD_OK;
+}
+
+mhd_status mhd_synchronize(mhd_mesh* m) {
+  if (!m) return fail(MHD_EINVAL, "null mesh");
+  CU(cudaStreamSynchronize(m->stream));
+  if (m->comm_stream) CU(cudaStreamSynchronize(m->comm_stream));
+  CU(cudaGetLastError());
+  return MHD_OK;
+}
+
+mhd_status mhd_set_kernel(mhd_mesh* m, int32_t variant) {
+  if (!m || variant < 0 || variant > 2) return fail(MHD_EINVAL, "variant must be 0, 1 or 2");
+  if (variant == 2) {
+    Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
+    const bool ok = m->info.dtype == MHD_F64 ? zmarch_supported<double>(m->g, full) : zmarch_supported<float>(m->g, full);
+    if (!ok) return fail(MHD_EUNSUPPORTED, "z-marching kernel does not support this geometry");
+  }
+  m->variant = variant;
+  return MHD_OK;
+}
+
+mhd_status mhd_mesh_query(const mhd_mesh* m, int32_t P[3], int32_t coord[3], int64_t local_n[3], int32_t* next_k) {
+  if (!m) return fail(MHD_EINVAL, "null mesh");
+  for (int a = 0; a < 3; ++a) {
+    if (P) P[a] = m->P[a];
+    if (coord) coord[a] = m->coord[a];
+    if (local_n) local_n[a] = m->L.n[a];
+  }
+  if (next_k) *next_k = m->next_k;
+  return MHD_OK;
+}
+
+mhd_status mhd_profile_enable(mhd_mesh* m, int32_t enable) {
+  if (!m) return fail(MHD_EINVAL, "null mesh");
+  CU(cudaStreamSynchronize(m->stream));
+  if (m->comm_stream) CU(cudaStreamSynchronize(m->comm_stream));
+  for (auto& v : m->recs) {
+    for (auto& r : v) {
+      m->pool.push_back(r.a);
+      m->pool.push_back(r.b);
+    }
+    v.clear();
+  }
+  m->prof = enable != 0;
+  return MHD_OK;
+}
+
+mhd_status mhd_profile_read(mhd_mesh* m, int32_t phase, int64_t* launches, double* ms, double* bytes) {
+  if (!m || phase < 0 || phase >= MHD_NPHASES) return fail(MHD_EINVAL, "bad profile_read argument");
+  CU(cudaStreamSynchronize(m->stream));
+  if (m->comm_stream) CU(cudaStreamSynchronize(m->comm_stream));
+  double tot = 0, by = 0;
+  for (auto& r : m->recs[phase]) {
+    float t = 0;
+    CU(cudaEventElapsedTime(&t, r.a, r.b));
+    tot += t;
+    by += r.bytes;
+  }
+  if (launches) *launches = (int64_t)m->recs[phase].size();
+  if (ms) *ms = tot;
+  if (bytes) *bytes = by;
+  return MHD_OK;
+}
+
+mhd_status mhd_launch_count(const mhd_mesh* m, int64_t* count) {
+  if (!m || !count) return fail(MHD_EINVAL, "null argument");
+  *count = m->launches;
+  return MHD_OK;
+}
+
+}  // extern "C"

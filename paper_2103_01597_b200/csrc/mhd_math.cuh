@@ -1,0 +1,252 @@
+// Per-cell arithmetic of the fused MHD substep: 6th-order derivatives in a fixed
+// canonical order, the RHS of Eqs. B.1-B.4 and the
+// Williamson 2N RK3 update.  Every update kernel (direct, z-marching,
+// inner/outer) evaluates exactly these operations in exactly this order, so a
+// cell's result is bit-identical whichever kernel or decomposition computed it.
+//
+// The library is compiled with -fmad=false: every fused multiply-add below is an
+// explicit fma(), nothing is contracted behind our back.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace b2 {
+
+constexpr int R = 3;   // stencil radius (Eq. 1); 6th order, k = 2r
+constexpr int NF = 8;  // lnrho, ux, uy, uz, s, Ax, Ay, Az (Table B.1; order R#14)
+enum { LNRHO = 0, UX = 1, UY = 2, UZ = 3, SS = 4, AX = 5, AY = 6, AZ = 7 };
+
+// Coefficients of one mesh, passed by value as a kernel parameter.
+// Stencil weights (readings R#1, R#2) are pre-divided by the grid spacing.
+template <typename T>
+struct Coef {
+  T c1[3][3];  // [axis][i-1]: first derivative  c_i / ds_a,          c = (3/4, -3/20, 1/60)
+  T d2[3][3];  // [axis][i-1]: second derivative d_i / ds_a^2,        d = (3/2, -3/20, 1/90)
+  T d0[3];     // [axis]:      centre weight    -49/18 / ds_a^2
+  T xw[3][3];  // [pair][i-1]: cross derivative e_i / (ds_a ds_b),     e = (270, -27, 2)/720
+               //              pairs 0 = (x,y), 1 = (x,z), 2 = (y,z)
+  // physics (Table B.2; EOS reading R#5, conduction R#6)
+  T gamma_cp, gm1, inv_cp, lnrho0, cs0sq, inv_T0, H_C, eta_inv_mu0, inv_mu0, nu, nu3, two_nu, zeta, eta, K;
+  // RK3 update: f_{k+1} = f_k + rkA[k] (f_k - f_{k-1}) + rkB[k] RHS  (R#3, R#4)
+  T rkA[3], rkB[3];
+};
+
+// All derivative quantities one cell needs.
+template <typename T>
+struct Derivs {
+  T f[NF];
+  T gl[3], gs[3];      // grad lnrho, grad s
+  T gu[3][3];          // gu[i][j] = d u_i / d x_j
+  T gA[3][3];          // gA[i][j] = d A_i / d x_j (i != j used)
+  T lapl, laps;        // Laplacians of lnrho and s
+  T d2u[3][3];         // d2u[i][j] = d^2 u_i / d x_j^2
+  T d2A[3][3];
+  T xu[3], xA[3];      // (grad div v)_i - d^2 v_i / d x_i^2 : the cross-derivative part
+};
+
+template <typename T> __device__ __forceinline__ T fma_(T a, T b, T c);
+template <> __device__ __forceinline__ double fma_<double>(double a, double b, double c) { return fma(a, b, c); }
+template <> __device__ __forceinline__ float fma_<float>(float a, float b, float c) { return fmaf(a, b, c); }
+template <typename T> __device__ __forceinline__ T exp_(T x);
+template <> __device__ __forceinline__ double exp_<double>(double x) { return exp(x); }
+template <> __device__ __forceinline__ float exp_<float>(float x) { return expf(x); }
+
+// ---- canonical operator forms -------------------------------------------------------------
+// D1 along an axis from the differences  Dl_i = f(+i) - f(-i)
+template <typename T>
+__device__ __forceinline__ T d1_of(T dl1, T dl2, T dl3, const T* c) {
+  return fma_(c[2], dl3, fma_(c[1], dl2, c[0] * dl1));
+}
+// D2 along an axis from the sums  Sg_i = f(+i) + f(-i)  and the centre value
+template <typename T>
+__device__ __forceinline__ T d2_of(T f0, T sg1, T sg2, T sg3, const T* d, T d0) {
+  return fma_(d[2], sg3, fma_(d[1], sg2, fma_(d[0], sg1, d0 * f0)));
+}
+
+// Accessor-driven gather of every derivative, in the canonical order.
+// V(q, dx, dy, dz) returns field q at the cell offset (dx, dy, dz).
+//
+// Cross derivatives (reading R#2; Eq. 14 point set):
+//   d_a d_b f = sum_{k=-3..3, k!=0} sgn(k) e_|k| / (ds_a ds_b) * Dl^a_|k|(f at +k e_b),
+// accumulated in increasing k (the z-marching kernel accumulates plane by plane in this
+// same order).  The graddiv cross parts are
+//   x_0 = d_x d_z v_z  (+ d_x d_y v_y inserted at k = 0)
+//   x_1 = d_y d_z v_z  (+ d_x d_y v_x inserted at k = 0)
+//   x_2 = d_x d_z v_x and d_y d_z v_y interleaved per k.
+template <typename T, class Acc>
+__device__ __forceinline__ void axis_pair(const Acc& V, int q, int a, const Coef<T>& C, T f0, T& d1, T& d2) {
+  const int ox = a == 0, oy = a == 1, oz = a == 2;
+  T p1 = V(q, ox, oy, oz), m1 = V(q, -ox, -oy, -oz);
+  T p2 = V(q, 2 * ox, 2 * oy, 2 * oz), m2 = V(q, -2 * ox, -2 * oy, -2 * oz);
+  T p3 = V(q, 3 * ox, 3 * oy, 3 * oz), m3 = V(q, -3 * ox, -3 * oy, -3 * oz);
+  d1 = d1_of(p1 - m1, p2 - m2, p3 - m3, C.c1[a]);
+  d2 = d2_of(f0, p1 + m1, p2 + m2, p3 + m3, C.d2[a], C.d0[a]);
+}
+
+// in-plane d_x d_y of field q (a = x, b = y)
+template <typename T, class Acc>
+__device__ __forceinline__ T cross_xy(const Acc& V, int q, const Coef<T>& C) {
+  const T* w = C.xw[0];
+  T acc = (-w[2]) * (V(q, 3, -3, 0) - V(q, -3, -3, 0));
+  acc = fma_(-w[1], V(q, 2, -2, 0) - V(q, -2, -2, 0), acc);
+  acc = fma_(-w[0], V(q, 1, -1, 0) - V(q, -1, -1, 0), acc);
+  acc = fma_(w[0], V(q, 1, 1, 0) - V(q, -1, 1, 0), acc);
+  acc = fma_(w[1], V(q, 2, 2, 0) - V(q, -2, 2, 0), acc);
+  acc = fma_(w[2], V(q, 3, 3, 0) - V(q, -3, 3, 0), acc);
+  return acc;
+}
+
+// Term of a z-cross at plane offset k (k != 0): Dl^a_|k|(f at +k e_z), a = 0 (x) or 1 (y)
+template <typename T, class Acc>
+__device__ __forceinline__ T zdelta(const Acc& V, int q, int a, int k) {
+  const int i = k < 0 ? -k : k;
+  return a == 0 ? V(q, i, 0, k) - V(q, -i, 0, k) : V(q, 0, i, k) - V(q, 0, -i, k);
+}
+template <typename T>
+__device__ __forceinline__ T zweight(const Coef<T>& C, int pair, int k) {
+  return k < 0 ? -C.xw[pair][-k - 1] : C.xw[pair][k - 1];
+}
+
+template <typename T, class Acc>
+__device__ __forceinline__ void cross_parts(const Acc& V, int qx, int qy, int qz, const Coef<T>& C, T x[3]) {
+  const T P0 = cross_xy<T>(V, qy, C);  // d_x d_y v_y
+  const T P1 = cross_xy<T>(V, qx, C);  // d_x d_y v_x
+  T a0 = zweight(C, 1, -3) * zdelta<T>(V, qz, 0, -3);
+  T a1 = zweight(C, 2, -3) * zdelta<T>(V, qz, 1, -3);
+  T a2 = zweight(C, 1, -3) * zdelta<T>(V, qx, 0, -3);
+  a2 = fma_(zweight(C, 2, -3), zdelta<T>(V, qy, 1, -3), a2);
+#pragma unroll
+  for (int k = -2; k <= 3; ++k) {
+    if (k == 0) {
+      a0 = a0 + P0;
+      a1 = a1 + P1;
+      continue;
+    }
+    a0 = fma_(zweight(C, 1, k), zdelta<T>(V, qz, 0, k), a0);
+    a1 = fma_(zweight(C, 2, k), zdelta<T>(V, qz, 1, k), a1);
+    a2 = fma_(zweight(C, 1, k), zdelta<T>(V, qx, 0, k), a2);
+    a2 = fma_(zweight(C, 2, k), zdelta<T>(V, qy, 1, k), a2);
+  }
+  x[0] = a0;
+  x[1] = a1;
+  x[2] = a2;
+}
+
+template <typename T, class Acc>
+__device__ __forceinline__ void gather(const Acc& V, const Coef<T>& C, Derivs<T>& D) {
+#pragma unroll
+  for (int q = 0; q < NF; ++q) D.f[q] = V(q, 0, 0, 0);
+  // lnrho and s: first derivatives and Laplacian (axis points only)
+  {
+    T d2x, d2y, d2z;
+    axis_pair<T>(V, LNRHO, 0, C, D.f[LNRHO], D.gl[0], d2x);
+    axis_pair<T>(V, LNRHO, 1, C, D.f[LNRHO], D.gl[1], d2y);
+    axis_pair<T>(V, LNRHO, 2, C, D.f[LNRHO], D.gl[2], d2z);
+    D.lapl = (d2x + d2y) + d2z;
+    axis_pair<T>(V, SS, 0, C, D.f[SS], D.gs[0], d2x);
+    axis_pair<T>(V, SS, 1, C, D.f[SS], D.gs[1], d2y);
+    axis_pair<T>(V, SS, 2, C, D.f[SS], D.gs[2], d2z);
+    D.laps = (d2x + d2y) + d2z;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      axis_pair<T>(V, UX + i, a, C, D.f[UX + i], D.gu[i][a], D.d2u[i][a]);
+      axis_pair<T>(V, AX + i, a, C, D.f[AX + i], D.gA[i][a], D.d2A[i][a]);
+    }
+  cross_parts<T>(V, UX, UY, UZ, C, D.xu);
+  cross_parts<T>(V, AX, AY, AZ, C, D.xA);
+}
+
+// ---- RHS of Eqs. B.1-B.4 -------------------------------------------------------
+// j = mu0^-1 (grad div A - lap A) (R#7); S traceless rate of shear (R#9); the rho in
+// 2 rho nu S:S and zeta rho (div u)^2 cancels against 1/(rho T).
+template <typename T>
+__device__ __forceinline__ void rhs_cell(const Derivs<T>& D, const Coef<T>& C, T out[NF]) {
+  const T lnrho = D.f[LNRHO], s = D.f[SS];
+  const T u0 = D.f[UX], u1 = D.f[UY], u2 = D.f[UZ];
+  const T divu = (D.gu[0][0] + D.gu[1][1]) + D.gu[2][2];
+  // B = curl A
+  const T B0 = D.gA[2][1] - D.gA[1][2];
+  const T B1 = D.gA[0][2] - D.gA[2][0];
+  const T B2 = D.gA[1][0] - D.gA[0][1];
+  // mu0 j = grad div A - lap A  (the d^2 A_i / dx_i^2 terms cancel exactly)
+  const T J0 = D.xA[0] - (D.d2A[0][1] + D.d2A[0][2]);
+  const T J1 = D.xA[1] - (D.d2A[1][0] + D.d2A[1][2]);
+  const T J2 = D.xA[2] - (D.d2A[2][0] + D.d2A[2][1]);
+  T lapA[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) lapA[i] = (D.d2A[i][0] + D.d2A[i][1]) + D.d2A[i][2];
+
+  // equation of state (R#5): theta = lnT - lnT0
+  const T theta = fma_(C.gamma_cp, s, C.gm1 * (lnrho - C.lnrho0));
+  const T inv_rho = exp_(-lnrho);
+  const T eth = exp_(theta);
+  const T cs2 = C.cs0sq * eth;
+  const T inv_T = C.inv_T0 / eth;
+
+  // (B.1) d lnrho/dt = -u.grad lnrho - div u
+  out[LNRHO] = -fma_(u2, D.gl[2], fma_(u1, D.gl[1], u0 * D.gl[0])) - divu;
+
+  // traceless rate of shear
+  const T divu3 = divu * (T)(1.0 / 3.0);
+  T S[3][3];
+  S[0][0] = D.gu[0][0] - divu3;
+  S[1][1] = D.gu[1][1] - divu3;
+  S[2][2] = D.gu[2][2] - divu3;
+  S[0][1] = S[1][0] = (T)0.5 * (D.gu[0][1] + D.gu[1][0]);
+  S[0][2] = S[2][0] = (T)0.5 * (D.gu[0][2] + D.gu[2][0]);
+  S[1][2] = S[2][1] = (T)0.5 * (D.gu[1][2] + D.gu[2][1]);
+
+  // (B.2) momentum
+  const T lor = inv_rho * C.inv_mu0;
+  const T jxB[3] = {J1 * B2 - J2 * B1, J2 * B0 - J0 * B2, J0 * B1 - J1 * B0};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const T adv = fma_(u2, D.gu[i][2], fma_(u1, D.gu[i][1], u0 * D.gu[i][0]));
+    const T pg = fma_(D.gs[i], C.inv_cp, D.gl[i]);
+    const T lapu = (D.d2u[i][0] + D.d2u[i][1]) + D.d2u[i][2];
+    const T gdu = D.d2u[i][i] + D.xu[i];
+    const T sgl = fma_(S[i][2], D.gl[2], fma_(S[i][1], D.gl[1], S[i][0] * D.gl[0]));
+    // nu (lap u + 1/3 grad div u + 2 S.grad lnrho) + zeta grad div u
+    const T visc = fma_(C.nu, lapu, fma_(C.two_nu, sgl, fma_(C.nu3, gdu, C.zeta * gdu)));
+    out[UX + i] = fma_(lor, jxB[i], fma_(-cs2, pg, visc - adv));
+  }
+
+  // (B.3) entropy: -u.grad s + [H - C + eta mu0 j^2]/(rho T) + [2 nu S:S + zeta (div u)^2]/T
+  //                + K/rho (lap theta + |grad theta|^2)
+  T SS2 = S[0][0] * S[0][0];
+  SS2 = fma_(S[1][1], S[1][1], SS2);
+  SS2 = fma_(S[2][2], S[2][2], SS2);
+  T off = S[0][1] * S[0][1];
+  off = fma_(S[0][2], S[0][2], off);
+  off = fma_(S[1][2], S[1][2], off);
+  SS2 = fma_((T)2, off, SS2);
+  const T J2s = fma_(J2, J2, fma_(J1, J1, J0 * J0));
+  const T gth0 = fma_(C.gamma_cp, D.gs[0], C.gm1 * D.gl[0]);
+  const T gth1 = fma_(C.gamma_cp, D.gs[1], C.gm1 * D.gl[1]);
+  const T gth2 = fma_(C.gamma_cp, D.gs[2], C.gm1 * D.gl[2]);
+  const T lapth = fma_(C.gamma_cp, D.laps, C.gm1 * D.lapl);
+  const T cond = C.K * inv_rho * fma_(gth2, gth2, fma_(gth1, gth1, fma_(gth0, gth0, lapth)));
+  const T ohm = fma_(C.eta_inv_mu0, J2s, C.H_C) * inv_rho;
+  const T visch = fma_(C.two_nu, SS2, C.zeta * divu * divu);
+  const T udgs = fma_(u2, D.gs[2], fma_(u1, D.gs[1], u0 * D.gs[0]));
+  out[SS] = fma_(ohm + visch, inv_T, cond - udgs);
+
+  // (B.4) dA/dt = u x B + eta lap A
+  out[AX] = fma_(C.eta, lapA[0], u1 * B2 - u2 * B1);
+  out[AY] = fma_(C.eta, lapA[1], u2 * B0 - u0 * B2);
+  out[AZ] = fma_(C.eta, lapA[2], u0 * B1 - u1 * B0);
+}
+
+// Williamson 2N RK3 with w reconstructed from two stored states (R#3, R#4):
+//   k = 0:  f1 = f0 + beta_0 dt RHS
+//   k > 0:  f_{k+1} = f_k + (beta_k alpha_k / beta_{k-1}) (f_k - f_{k-1}) + beta_k dt RHS
+template <typename T>
+__device__ __forceinline__ T rk_update(int k, T fk, T fprev, T rhs, const Coef<T>& C) {
+  const T t = fma_(C.rkB[k], rhs, fk);
+  return k == 0 ? t : fma_(C.rkA[k], fk - fprev, t);
+}
+
+}  // namespace b2

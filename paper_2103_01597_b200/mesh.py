@@ -1,0 +1,132 @@
+"""`Mesh`: one rank's subdomain, its device workspace and stream (argument marshalling only).
+
+All arithmetic runs in libb2mhd.so; this class allocates the caller-owned workspace
+(a torch uint8 tensor), picks the stream, broadcasts the NCCL unique id over the
+torch process group, and moves tensors in and out through the C ABI.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as native
+
+_TORCH_DT = {native.MHD_F64: "float64", native.MHD_F32: "float32"}
+
+
+class Mesh:
+    def __init__(self, n_xyz, ds_xyz, params: dict, dtype: int = native.MHD_F64, rank: int = 0, nranks: int = 1,
+                 exchange_corners: bool = False, stream=None, process_group=None, kernel: int = 0):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("b2mhd needs a CUDA device (no CPU fallback)")
+        self.torch = torch
+        self.dtype = int(dtype)
+        self.tdtype = getattr(torch, _TORCH_DT[self.dtype])
+        self.info = native.make_info(n_xyz, ds_xyz, params, dtype, rank, nranks, exchange_corners)
+        self.nbytes = native.mhd_workspace_bytes(self.info)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+        self.workspace = torch.empty(self.nbytes, dtype=torch.uint8, device=self.device)
+        self.handle = native.mhd_mesh_create(self.info, self.workspace.data_ptr(), self.nbytes,
+                                             self.stream.cuda_stream)
+        self.P, self.coord, self.local_n, _ = native.mhd_mesh_query(self.handle)
+        self.shape = (self.local_n[2], self.local_n[1], self.local_n[0])  # (nz', ny', nx')
+        if nranks > 1:
+            import torch.distributed as dist
+            obj = [native.mhd_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=process_group)
+            native.mhd_comm_init(self.handle, obj[0])
+        if kernel:
+            native.mhd_set_kernel(self.handle, kernel)
+
+    # ---- state I/O ----------------------------------------------------------------------------
+    def _dt_of(self, t) -> int:
+        return native.MHD_F64 if t.dtype in (self.torch.float64, np.float64) else native.MHD_F32
+
+    def load(self, state) -> None:
+        """state: (8, nz', ny', nx') torch tensor (device or host) or numpy array, C-contiguous."""
+        torch = self.torch
+        if isinstance(state, np.ndarray):
+            state = torch.from_numpy(np.ascontiguousarray(state))
+        assert tuple(state.shape) == (8,) + tuple(self.shape), (state.shape, self.shape)
+        state = state.contiguous()
+        on_dev = state.is_cuda
+        if on_dev:
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        dt = self._dt_of(state)
+        for q in range(8):
+            native.mhd_load(self.handle, q, state[q].data_ptr(), dt, on_dev)
+        if not on_dev:
+            self.synchronize()  # the host buffer may be reused by the caller
+        self._keep = state
+
+    def store(self, out=None, dtype=None):
+        """Returns (8, nz', ny', nx'); `out` may be a device or (pinned) host tensor."""
+        torch = self.torch
+        if out is None:
+            out = torch.empty((8,) + tuple(self.shape), dtype=dtype or self.tdtype, device=self.device)
+        on_dev = out.is_cuda
+        dt = self._dt_of(out)
+        for q in range(8):
+            native.mhd_store(self.handle, q, out[q].data_ptr(), dt, on_dev)
+        if on_dev:
+            torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        return out
+
+    def store_grid(self):
+        """Halo-inclusive local grids, (8, nz'+6, ny'+6, nx'+6), on the host (test hook)."""
+        sh = tuple(v + 6 for v in self.shape)
+        out = self.torch.empty((8,) + sh, dtype=self.tdtype).pin_memory()
+        for q in range(8):
+            native.mhd_store_grid(self.handle, q, out[q].data_ptr(), False)
+        return out
+
+    # ---- hot path -------------------------------------------------------------------------------
+    def halo_exchange(self) -> None:
+        native.mhd_halo_exchange(self.handle)
+
+    def substep(self, k: int, dt: float) -> None:
+        native.mhd_integrate_substep(self.handle, k, dt)
+
+    def step(self, dt: float) -> None:
+        native.mhd_integrate_step(self.handle, dt)
+
+    def reduce(self, field: int, op: int, allow_nonfinite: bool = False) -> float:
+        return native.mhd_reduce(self.handle, field, op, allow_nonfinite)
+
+    def debug_rhs(self):
+        out = self.torch.empty((8,) + tuple(self.shape), dtype=self.tdtype, device=self.device)
+        native.mhd_debug_rhs(self.handle, out.data_ptr())
+        self.torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        return out
+
+    def set_kernel(self, variant: int) -> None:
+        native.mhd_set_kernel(self.handle, variant)
+
+    def synchronize(self) -> None:
+        native.mhd_synchronize(self.handle)
+
+    def profile(self, enable: bool) -> None:
+        native.mhd_profile_enable(self.handle, enable)
+
+    def profile_read(self) -> dict:
+        out = {}
+        for i, name in enumerate(native.PHASES):
+            n, ms, by = native.mhd_profile_read(self.handle, i)
+            out[name] = dict(launches=n, ms=ms, bytes=by)
+        return out
+
+    def launch_count(self) -> int:
+        return native.mhd_launch_count(self.handle)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            native.mhd_mesh_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -8,7 +8,19 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def _build_native():
+    """Compile libb2mhd.so and the oracle before anything imports the package (which loads the .so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_b2_build", os.path.join(ROOT, "paper_2103_01597_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()
+    import oracle
+    oracle.build()
+
+
 def pytest_configure(config):
+    _build_native()
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
