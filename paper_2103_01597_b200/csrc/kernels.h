@@ -1,7 +1,10 @@
 // Internal (non-ABI) declarations shared by the runtime (mesh.cpp) and the kernels.
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime driver entry point)
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "mhd_math.cuh"
 
@@ -54,12 +57,28 @@ void launch_copy_out(cudaStream_t st, const TS* origin, TD* dst, const Geom& g);
 template <typename T>
 void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scratch, int nblocks);
 
-// ---- z-marching shared-memory kernel (zmarch.cu) ----
+// ---- z-marching TMA kernel (zmarch.cu) ----
+// Tile of a CTA and the TMA boxes it stages per plane and field.  TMA requires the innermost
+// start coordinate to be 16-byte aligned, so boxes start at x rounded down to 16 bytes and are
+// widened accordingly: halo box COLS x ROWS x 1 from (floor16(x0 - 3), y0 - 3, z), f_{k-1} box
+// PCOLS x TY x 1 from (floor16(x0), y0, z).
+constexpr int kZTX = 32, kZTY = 8;
+template <typename T>
+constexpr int zm_ch() { return 16 / (int)sizeof(T); }
+template <typename T>
+constexpr int zm_cols() { return (kZTX + 6 + zm_ch<T>() - 1 + zm_ch<T>() - 1) / zm_ch<T>() * zm_ch<T>(); }
+template <typename T>
+constexpr int zm_pcols() { return kZTX + zm_ch<T>(); }
+constexpr int zm_rows() { return kZTY + 6; }
+struct TmapSet {
+  CUtensorMap halo[NF];  // fields of the state read with the stencil
+  CUtensorMap prev[NF];  // fields of the other state (f_{k-1}, read pointwise)
+};
 template <typename T>
 bool zmarch_supported(const Geom& g, const Region& r);
 template <typename T>
-void launch_zmarch(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, const Geom& g,
-                   const Region& r, const Coef<T>& C, int k, T* rhs_out);
+void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
+                   const Coef<T>& C, int k, T* rhs_out, int xo);
 
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 constexpr int kReduceVals = 5;      // min, max, sum, sum of squares, sum of exp

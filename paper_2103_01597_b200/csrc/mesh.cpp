@@ -8,6 +8,8 @@
 //    exchange there, the inner-segment update concurrently on the compute stream, then
 //    unpack -> event -> outer segments.  Stream order replaces the paper's per-iteration
 //    cudaDeviceSynchronize + MPI_Barrier.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -212,7 +214,8 @@ Layout make_layout(const mhd_mesh_info* info, int rank, const std::vector<SegInf
   L.xo = al;
   L.sy = (int64_t)align_up((size_t)(L.xo + L.n[0] + MHD_RADIUS + 1), (size_t)al);
   L.sz = L.sy * (L.n[1] + 2 * MHD_RADIUS);
-  L.field_elems = (int64_t)align_up((size_t)(L.sz * (L.n[2] + 2 * MHD_RADIUS) + 2 * al), (size_t)(256 / es));
+  // + one row and a chunk of slack: tiled kernels may over-read (never use) past the last halo row
+  L.field_elems = (int64_t)align_up((size_t)(L.sz * (L.n[2] + 2 * MHD_RADIUS) + L.sy + 4 * al), (size_t)(256 / es));
   L.origin = MHD_RADIUS * L.sz + MHD_RADIUS * L.sy + L.xo;
   L.field_bytes = (size_t)L.field_elems * es;
   size_t off = 0;
@@ -263,6 +266,8 @@ struct mhd_mesh {
   int variant = 0;
   int64_t launches = 0;
   double* h_red = nullptr;  // pinned
+  TmapSet tmaps[2];          // [state read with the stencil]
+  bool tmaps_ok = false;
   // profiling: (start, stop) event pairs per phase, with the algorithmic bytes of the launch
   struct Rec {
     cudaEvent_t a, b;
@@ -327,6 +332,43 @@ SegList make_list(const mhd_mesh& m, bool self, bool send) {
   return Ls;
 }
 
+// TMA descriptors of the z-marching kernel: per state and field, a 3-D view
+// (x: row pitch sy, y: ny + 6 rows, z: nz + 6 planes) of the pitched field, with the halo box
+// and the f_{k-1} box of the kernel's tile.
+mhd_status encode_tmaps(mhd_mesh* m) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return fail(MHD_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const bool f64 = m->info.dtype == MHD_F64;
+  const size_t es = (size_t)m->info.dtype;
+  const cuuint64_t dims[3] = {(cuuint64_t)m->L.sy, (cuuint64_t)(m->g.ny + 2 * MHD_RADIUS),
+                              (cuuint64_t)(m->g.nz + 2 * MHD_RADIUS)};
+  const cuuint64_t strides[2] = {(cuuint64_t)(m->L.sy * es), (cuuint64_t)(m->L.sz * es)};
+  const cuuint32_t halo_box[3] = {(cuuint32_t)(f64 ? zm_cols<double>() : zm_cols<float>()), (cuuint32_t)zm_rows(), 1};
+  const cuuint32_t prev_box[3] = {(cuuint32_t)(f64 ? zm_pcols<double>() : zm_pcols<float>()), (cuuint32_t)kZTY, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  for (int s = 0; s < 2; ++s)
+    for (int q = 0; q < NF; ++q) {
+      for (int which = 0; which < 2; ++which) {
+        const int state = which == 0 ? s : 1 - s;
+        void* base = m->ws + m->L.state_off[state] + (size_t)q * m->L.field_bytes;
+        CUtensorMap* map = which == 0 ? &m->tmaps[s].halo[q] : &m->tmaps[s].prev[q];
+        CUresult r = encode(map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims,
+                            strides, which == 0 ? halo_box : prev_box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(MHD_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+      }
+    }
+  m->tmaps_ok = true;
+  return MHD_OK;
+}
+
 // Phase timer: records a start event now and the stop event when it goes out of scope.
 struct PhaseTimer {
   mhd_mesh* m;
@@ -359,11 +401,11 @@ template <typename T>
 void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out) {
   const Fields<T> in = m->fields<T>(m->cur), out = m->fields<T>(1 - m->cur);
   const Coef<T> C = make_coef<T>(m->info, k, dt);
-  const bool zm = m->variant != 1 && zmarch_supported<T>(m->g, r);
+  const bool zm = m->variant != 1 && m->tmaps_ok && zmarch_supported<T>(m->g, r);
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
   PhaseTimer t(m, m->stream, MHD_PHASE_UPDATE, cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
   if (zm)
-    launch_zmarch<T>(m->stream, in, out, m->g, r, C, k, rhs_out);
+    launch_zmarch<T>(m->stream, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo);
   else
     launch_direct<T>(m->stream, in, out, m->g, r, C, k, rhs_out);
   m->launches++;
@@ -643,6 +685,11 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
     delete m;
     return fail(MHD_ECUDA, std::string("mesh create: ") + cudaGetErrorString(e));
   }
+  st = encode_tmaps(m);
+  if (st != MHD_OK) {
+    delete m;
+    return st;
+  }
   *out = m;
   return MHD_OK;
 }
@@ -791,7 +838,8 @@ mhd_status mhd_set_kernel(mhd_mesh* m, int32_t variant) {
   if (!m || variant < 0 || variant > 2) return fail(MHD_EINVAL, "variant must be 0, 1 or 2");
   if (variant == 2) {
     Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
-    const bool ok = m->info.dtype == MHD_F64 ? zmarch_supported<double>(m->g, full) : zmarch_supported<float>(m->g, full);
+    const bool ok = m->tmaps_ok && (m->info.dtype == MHD_F64 ? zmarch_supported<double>(m->g, full)
+                                                            : zmarch_supported<float>(m->g, full));
     if (!ok) return fail(MHD_EUNSUPPORTED, "z-marching kernel does not support this geometry");
   }
   m->variant = variant;

@@ -162,22 +162,37 @@ __device__ __forceinline__ void gather(const Acc& V, const Coef<T>& C, Derivs<T>
 // ---- RHS of Eqs. B.1-B.4 -------------------------------------------------------
 // j = mu0^-1 (grad div A - lap A) (R#7); S traceless rate of shear (R#9); the rho in
 // 2 rho nu S:S and zeta rho (div u)^2 cancels against 1/(rho T).
+// Split in stages so a kernel may contract the magnetic derivatives as soon as they exist;
+// every kernel evaluates the same expressions, so values are identical wherever they run.
 template <typename T>
-__device__ __forceinline__ void rhs_cell(const Derivs<T>& D, const Coef<T>& C, T out[NF]) {
-  const T lnrho = D.f[LNRHO], s = D.f[SS];
-  const T u0 = D.f[UX], u1 = D.f[UY], u2 = D.f[UZ];
-  const T divu = (D.gu[0][0] + D.gu[1][1]) + D.gu[2][2];
-  // B = curl A
-  const T B0 = D.gA[2][1] - D.gA[1][2];
-  const T B1 = D.gA[0][2] - D.gA[2][0];
-  const T B2 = D.gA[1][0] - D.gA[0][1];
+struct MagPart {
+  T B[3], J[3], lapA[3];  // B = curl A, J = mu0 j, lap A
+};
+
+template <typename T>
+__device__ __forceinline__ MagPart<T> mag_part(const T (&gA)[3][3], const T (&d2A)[3][3], const T (&xA)[3]) {
+  MagPart<T> m;
+  m.B[0] = gA[2][1] - gA[1][2];
+  m.B[1] = gA[0][2] - gA[2][0];
+  m.B[2] = gA[1][0] - gA[0][1];
   // mu0 j = grad div A - lap A  (the d^2 A_i / dx_i^2 terms cancel exactly)
-  const T J0 = D.xA[0] - (D.d2A[0][1] + D.d2A[0][2]);
-  const T J1 = D.xA[1] - (D.d2A[1][0] + D.d2A[1][2]);
-  const T J2 = D.xA[2] - (D.d2A[2][0] + D.d2A[2][1]);
-  T lapA[3];
+  m.J[0] = xA[0] - (d2A[0][1] + d2A[0][2]);
+  m.J[1] = xA[1] - (d2A[1][0] + d2A[1][2]);
+  m.J[2] = xA[2] - (d2A[2][0] + d2A[2][1]);
 #pragma unroll
-  for (int i = 0; i < 3; ++i) lapA[i] = (D.d2A[i][0] + D.d2A[i][1]) + D.d2A[i][2];
+  for (int i = 0; i < 3; ++i) m.lapA[i] = (d2A[i][0] + d2A[i][1]) + d2A[i][2];
+  return m;
+}
+
+// Everything but the magnetic contraction.  u, lnrho, s are the cell values.
+template <typename T>
+__device__ __forceinline__ void rhs_rest(T lnrho, T s, const T (&u)[3], const T (&gl)[3], const T (&gs)[3],
+                                         const T (&gu)[3][3], T lapl, T laps, const T (&d2u)[3][3], const T (&xu)[3],
+                                         const MagPart<T>& m, const Coef<T>& C, T out[NF]) {
+  const T u0 = u[0], u1 = u[1], u2 = u[2];
+  const T divu = (gu[0][0] + gu[1][1]) + gu[2][2];
+  const T B0 = m.B[0], B1 = m.B[1], B2 = m.B[2];
+  const T J0 = m.J[0], J1 = m.J[1], J2 = m.J[2];
 
   // equation of state (R#5): theta = lnT - lnT0
   const T theta = fma_(C.gamma_cp, s, C.gm1 * (lnrho - C.lnrho0));
@@ -187,28 +202,28 @@ __device__ __forceinline__ void rhs_cell(const Derivs<T>& D, const Coef<T>& C, T
   const T inv_T = C.inv_T0 / eth;
 
   // (B.1) d lnrho/dt = -u.grad lnrho - div u
-  out[LNRHO] = -fma_(u2, D.gl[2], fma_(u1, D.gl[1], u0 * D.gl[0])) - divu;
+  out[LNRHO] = -fma_(u2, gl[2], fma_(u1, gl[1], u0 * gl[0])) - divu;
 
   // traceless rate of shear
   const T divu3 = divu * (T)(1.0 / 3.0);
   T S[3][3];
-  S[0][0] = D.gu[0][0] - divu3;
-  S[1][1] = D.gu[1][1] - divu3;
-  S[2][2] = D.gu[2][2] - divu3;
-  S[0][1] = S[1][0] = (T)0.5 * (D.gu[0][1] + D.gu[1][0]);
-  S[0][2] = S[2][0] = (T)0.5 * (D.gu[0][2] + D.gu[2][0]);
-  S[1][2] = S[2][1] = (T)0.5 * (D.gu[1][2] + D.gu[2][1]);
+  S[0][0] = gu[0][0] - divu3;
+  S[1][1] = gu[1][1] - divu3;
+  S[2][2] = gu[2][2] - divu3;
+  S[0][1] = S[1][0] = (T)0.5 * (gu[0][1] + gu[1][0]);
+  S[0][2] = S[2][0] = (T)0.5 * (gu[0][2] + gu[2][0]);
+  S[1][2] = S[2][1] = (T)0.5 * (gu[1][2] + gu[2][1]);
 
   // (B.2) momentum
   const T lor = inv_rho * C.inv_mu0;
   const T jxB[3] = {J1 * B2 - J2 * B1, J2 * B0 - J0 * B2, J0 * B1 - J1 * B0};
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const T adv = fma_(u2, D.gu[i][2], fma_(u1, D.gu[i][1], u0 * D.gu[i][0]));
-    const T pg = fma_(D.gs[i], C.inv_cp, D.gl[i]);
-    const T lapu = (D.d2u[i][0] + D.d2u[i][1]) + D.d2u[i][2];
-    const T gdu = D.d2u[i][i] + D.xu[i];
-    const T sgl = fma_(S[i][2], D.gl[2], fma_(S[i][1], D.gl[1], S[i][0] * D.gl[0]));
+    const T adv = fma_(u2, gu[i][2], fma_(u1, gu[i][1], u0 * gu[i][0]));
+    const T pg = fma_(gs[i], C.inv_cp, gl[i]);
+    const T lapu = (d2u[i][0] + d2u[i][1]) + d2u[i][2];
+    const T gdu = d2u[i][i] + xu[i];
+    const T sgl = fma_(S[i][2], gl[2], fma_(S[i][1], gl[1], S[i][0] * gl[0]));
     // nu (lap u + 1/3 grad div u + 2 S.grad lnrho) + zeta grad div u
     const T visc = fma_(C.nu, lapu, fma_(C.two_nu, sgl, fma_(C.nu3, gdu, C.zeta * gdu)));
     out[UX + i] = fma_(lor, jxB[i], fma_(-cs2, pg, visc - adv));
@@ -224,20 +239,27 @@ __device__ __forceinline__ void rhs_cell(const Derivs<T>& D, const Coef<T>& C, T
   off = fma_(S[1][2], S[1][2], off);
   SS2 = fma_((T)2, off, SS2);
   const T J2s = fma_(J2, J2, fma_(J1, J1, J0 * J0));
-  const T gth0 = fma_(C.gamma_cp, D.gs[0], C.gm1 * D.gl[0]);
-  const T gth1 = fma_(C.gamma_cp, D.gs[1], C.gm1 * D.gl[1]);
-  const T gth2 = fma_(C.gamma_cp, D.gs[2], C.gm1 * D.gl[2]);
-  const T lapth = fma_(C.gamma_cp, D.laps, C.gm1 * D.lapl);
+  const T gth0 = fma_(C.gamma_cp, gs[0], C.gm1 * gl[0]);
+  const T gth1 = fma_(C.gamma_cp, gs[1], C.gm1 * gl[1]);
+  const T gth2 = fma_(C.gamma_cp, gs[2], C.gm1 * gl[2]);
+  const T lapth = fma_(C.gamma_cp, laps, C.gm1 * lapl);
   const T cond = C.K * inv_rho * fma_(gth2, gth2, fma_(gth1, gth1, fma_(gth0, gth0, lapth)));
   const T ohm = fma_(C.eta_inv_mu0, J2s, C.H_C) * inv_rho;
   const T visch = fma_(C.two_nu, SS2, C.zeta * divu * divu);
-  const T udgs = fma_(u2, D.gs[2], fma_(u1, D.gs[1], u0 * D.gs[0]));
+  const T udgs = fma_(u2, gs[2], fma_(u1, gs[1], u0 * gs[0]));
   out[SS] = fma_(ohm + visch, inv_T, cond - udgs);
 
   // (B.4) dA/dt = u x B + eta lap A
-  out[AX] = fma_(C.eta, lapA[0], u1 * B2 - u2 * B1);
-  out[AY] = fma_(C.eta, lapA[1], u2 * B0 - u0 * B2);
-  out[AZ] = fma_(C.eta, lapA[2], u0 * B1 - u1 * B0);
+  out[AX] = fma_(C.eta, m.lapA[0], u1 * B2 - u2 * B1);
+  out[AY] = fma_(C.eta, m.lapA[1], u2 * B0 - u0 * B2);
+  out[AZ] = fma_(C.eta, m.lapA[2], u0 * B1 - u1 * B0);
+}
+
+template <typename T>
+__device__ __forceinline__ void rhs_cell(const Derivs<T>& D, const Coef<T>& C, T out[NF]) {
+  const MagPart<T> m = mag_part<T>(D.gA, D.d2A, D.xA);
+  const T u[3] = {D.f[UX], D.f[UY], D.f[UZ]};
+  rhs_rest<T>(D.f[LNRHO], D.f[SS], u, D.gl, D.gs, D.gu, D.lapl, D.laps, D.d2u, D.xu, m, C, out);
 }
 
 // Williamson 2N RK3 with w reconstructed from two stored states (R#3, R#4):

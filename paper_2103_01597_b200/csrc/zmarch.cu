@@ -1,13 +1,385 @@
-// z-marching shared-memory update kernel (placeholder until the tiled kernel lands).
+// z-marching update kernel: the hot path on sm_100a.
+//
+// A CTA owns a TX x TY column of cells and marches it along z over a chunk of planes.
+//  * Staging: each plane (8 fields, tile + radius-3 halo in x and y) is fetched by TMA
+//    (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion) into a 5-slot
+//    shared-memory ring, one plane ahead of the computation; f_{k-1} of the output plane
+//    (read pointwise by the RK3 update) rides in the same transaction.  One CTA barrier per
+//    plane protects slot reuse.
+//  * In-plane derivatives (x, y axes and the d_x d_y diagonals of Eq. 14) are read
+//    from the slot of the output plane o; the z column of every field comes from registers
+//    (planes o-3..o-1) and from the ring (o+1..o+3).
+//  * The d_x d_z / d_y d_z cross terms are split: the k < 0 half is PUSHED from each plane into
+//    register accumulators of the next three outputs, reusing that plane's own x/y differences;
+//    the k > 0 half is PULLED from the ring.  This reproduces mhd_math.cuh::cross_parts term by
+//    term, so the result is bit-identical to the direct kernel
+//    (tests/test_gpu_parity.py::test_kernel_variants_bit_identical).
+//  * Fields are processed one vector at a time (A, then u, then lnrho and s) and the magnetic
+//    derivatives are contracted to B, mu0 j and lap A as soon as they exist, to keep the live
+//    register set small.  The march is unrolled by 3 so the register history rotates by
+//    renaming, not by moves.
 #include "kernels.h"
 
 namespace b2 {
+
+namespace {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, int TX, int TY>
+struct ZCfg {
+  static constexpr int ES = (int)sizeof(T);
+  static constexpr int COLS = zm_cols<T>();
+  static constexpr int ROWS = TY + 6;
+  static constexpr int FSZ = (ROWS * COLS * ES + 127) / 128 * 128 / ES;  // 128-B aligned TMA destinations
+  static constexpr int SLOT = NF * FSZ;
+  static constexpr int NSLOT = 5;
+  static constexpr int NT = TX * TY;
+  static constexpr int CH = zm_ch<T>();
+  static constexpr int PCOLS = zm_pcols<T>();
+  static constexpr int PSZ = (TY * PCOLS * ES + 127) / 128 * 128 / ES;  // f_{k-1} tile per field
+  static constexpr unsigned HALO_TX = (unsigned)(NF * ROWS * COLS * ES);
+  static constexpr unsigned PREV_TX = (unsigned)(NF * TY * PCOLS * ES);
+  static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128 + 128;
+};
+
+// Register state carried along z by one thread.
 template <typename T>
-bool zmarch_supported(const Geom&, const Region&) { return false; }
+struct March {
+  T hist[NF][3];   // physical storage of f(o-3), f(o-2), f(o-1); logical index j at phase PH is (j + PH) % 3
+  T acc[2][3][3];  // [u|A][logical output o, o+1, o+2 -> physical (j + PH) % 3][z-part of x_0, x_1, x_2]
+};
+
+template <typename T, int TX, int TY, int MODE>
+struct ZStep {
+  using Z = ZCfg<T, TX, TY>;
+  const T* ring;
+  const T* prevbuf;
+  const Coef<T>& C;
+  int cell;   // offset of this thread's cell inside a field of a slot
+  int pcell;  // offset inside a field of the f_{k-1} tile
+  int slot0;  // plane zb - 3 (first staged plane) has slot 0
+
+  __device__ __forceinline__ const T* slot_of(int plane) const {
+    return ring + ((plane - slot0) % Z::NSLOT) * Z::SLOT + cell;
+  }
+  static __device__ __forceinline__ T at(const T* sp, int q, int dx, int dy) {
+    return sp[q * Z::FSZ + dy * Z::COLS + dx];
+  }
+
+  // x/y first and second derivatives of field q in the slot, with the differences kept
+  __device__ __forceinline__ void axis_xy(const T* sp, int q, T f0, T (&d1)[2], T (&d2)[2], T (&dlx)[3],
+                                          T (&dly)[3]) const {
+    T sg[2][3];
+#pragma unroll
+    for (int i = 1; i <= 3; ++i) {
+      const T px = at(sp, q, i, 0), mx = at(sp, q, -i, 0);
+      const T py = at(sp, q, 0, i), my = at(sp, q, 0, -i);
+      dlx[i - 1] = px - mx;
+      sg[0][i - 1] = px + mx;
+      dly[i - 1] = py - my;
+      sg[1][i - 1] = py + my;
+    }
+    d1[0] = d1_of(dlx[0], dlx[1], dlx[2], C.c1[0]);
+    d2[0] = d2_of(f0, sg[0][0], sg[0][1], sg[0][2], C.d2[0], C.d0[0]);
+    d1[1] = d1_of(dly[0], dly[1], dly[2], C.c1[1]);
+    d2[1] = d2_of(f0, sg[1][0], sg[1][1], sg[1][2], C.d2[1], C.d0[1]);
+  }
+  // z derivatives from the column
+  template <int PH>
+  __device__ __forceinline__ void axis_z(const March<T>& st, int q, T f0, T p1, T p2, T p3, T& d1, T& d2) const {
+    const T m1 = st.hist[q][(2 + PH) % 3], m2 = st.hist[q][(1 + PH) % 3], m3 = st.hist[q][(0 + PH) % 3];
+    d1 = d1_of(p1 - m1, p2 - m2, p3 - m3, C.c1[2]);
+    d2 = d2_of(f0, p1 + m1, p2 + m2, p3 + m3, C.d2[2], C.d0[2]);
+  }
+  __device__ __forceinline__ T cross_xy_s(const T* sp, int q) const {
+    const T* w = C.xw[0];
+    T a = (-w[2]) * (at(sp, q, 3, -3) - at(sp, q, -3, -3));
+    a = fma_(-w[1], at(sp, q, 2, -2) - at(sp, q, -2, -2), a);
+    a = fma_(-w[0], at(sp, q, 1, -1) - at(sp, q, -1, -1), a);
+    a = fma_(w[0], at(sp, q, 1, 1) - at(sp, q, -1, 1), a);
+    a = fma_(w[1], at(sp, q, 2, 2) - at(sp, q, -2, 2), a);
+    a = fma_(w[2], at(sp, q, 3, 3) - at(sp, q, -3, 3), a);
+    return a;
+  }
+  // k < 0 half of the z-cross terms of plane p for vector v: outputs p+1 (k = -1), p+2 (k = -2),
+  // and a fresh accumulator for p+3 (k = -3), which lands in the physical slot of output p.
+  template <int PH>
+  __device__ __forceinline__ void push(March<T>& st, int v, const T (&dlx_x)[3], const T (&dly_y)[3],
+                                       const T (&dlx_z)[3], const T (&dly_z)[3]) const {
+    const T* wxz = C.xw[1];
+    const T* wyz = C.xw[2];
+#pragma unroll
+    for (int j = 1; j <= 2; ++j) {
+      T* a = st.acc[v][(j + PH) % 3];
+      a[0] = fma_(-wxz[j - 1], dlx_z[j - 1], a[0]);
+      a[1] = fma_(-wyz[j - 1], dly_z[j - 1], a[1]);
+      a[2] = fma_(-wxz[j - 1], dlx_x[j - 1], a[2]);
+      a[2] = fma_(-wyz[j - 1], dly_y[j - 1], a[2]);
+    }
+    T* f = st.acc[v][(0 + PH) % 3];
+    f[0] = (-wxz[2]) * dlx_z[2];
+    f[1] = (-wyz[2]) * dly_z[2];
+    f[2] = fma_(-wyz[2], dly_y[2], (-wxz[2]) * dlx_x[2]);
+  }
+
+  // push-only pass over a plane below the chunk (prologue)
+  template <int PH>
+  __device__ __forceinline__ void push_only(March<T>& st, int p) const {
+    const T* s0 = slot_of(p);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int qx = v == 0 ? UX : AX;
+      T dlx_x[3], dly_y[3], dlx_z[3], dly_z[3];
+#pragma unroll
+      for (int i = 1; i <= 3; ++i) {
+        dlx_x[i - 1] = at(s0, qx, i, 0) - at(s0, qx, -i, 0);
+        dly_y[i - 1] = at(s0, qx + 1, 0, i) - at(s0, qx + 1, 0, -i);
+        dlx_z[i - 1] = at(s0, qx + 2, i, 0) - at(s0, qx + 2, -i, 0);
+        dly_z[i - 1] = at(s0, qx + 2, 0, i) - at(s0, qx + 2, 0, -i);
+      }
+      push<PH>(st, v, dlx_x, dly_y, dlx_z, dly_z);
+    }
+#pragma unroll
+    for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % 3] = at(s0, q, 0, 0);
+  }
+
+  // Derivatives of one vector field (u or A) at output plane o: first and second derivatives
+  // along every axis, the graddiv cross parts, and the push of plane o's differences.
+  template <int PH>
+  __device__ __forceinline__ void vector_derivs(March<T>& st, int v, const T* s0, const T* s1, const T* s2,
+                                                const T* s3, T (&f)[3], T (&g)[3][3], T (&d2)[3][3],
+                                                T (&x)[3]) const {
+    const int qx = v == 0 ? UX : AX;
+    T dlx[3][3], dly[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int q = qx + c;
+      f[c] = at(s0, q, 0, 0);
+      T d1a[2], d2a[2];
+      axis_xy(s0, q, f[c], d1a, d2a, dlx[c], dly[c]);
+      g[c][0] = d1a[0];
+      g[c][1] = d1a[1];
+      d2[c][0] = d2a[0];
+      d2[c][1] = d2a[1];
+      axis_z<PH>(st, q, f[c], at(s1, q, 0, 0), at(s2, q, 0, 0), at(s3, q, 0, 0), g[c][2], d2[c][2]);
+    }
+    // graddiv cross parts: k < 0 (accumulated), + in-plane part at k = 0, then k = 1, 2, 3
+    const T P0 = cross_xy_s(s0, qx + 1);  // d_x d_y v_y
+    const T P1 = cross_xy_s(s0, qx);      // d_x d_y v_x
+    const T* a = st.acc[v][(0 + PH) % 3];
+    x[0] = a[0] + P0;
+    x[1] = a[1] + P1;
+    x[2] = a[2];
+    const T* wxz = C.xw[1];
+    const T* wyz = C.xw[2];
+#pragma unroll
+    for (int kk = 1; kk <= 3; ++kk) {
+      const T* sk = kk == 1 ? s1 : (kk == 2 ? s2 : s3);
+      x[0] = fma_(wxz[kk - 1], at(sk, qx + 2, kk, 0) - at(sk, qx + 2, -kk, 0), x[0]);
+      x[1] = fma_(wyz[kk - 1], at(sk, qx + 2, 0, kk) - at(sk, qx + 2, 0, -kk), x[1]);
+      x[2] = fma_(wxz[kk - 1], at(sk, qx, kk, 0) - at(sk, qx, -kk, 0), x[2]);
+      x[2] = fma_(wyz[kk - 1], at(sk, qx + 1, 0, kk) - at(sk, qx + 1, 0, -kk), x[2]);
+    }
+    push<PH>(st, v, dlx[0], dly[1], dlx[2], dly[2]);
+  }
+
+  template <int PH>
+  __device__ __forceinline__ void full(March<T>& st, int o, const Fields<T>& out, const Geom& g, int k, bool active,
+                                       int x, int y, T* rhs_out) const {
+    const T* s0 = slot_of(o);
+    const T* s1 = slot_of(o + 1);
+    const T* s2 = slot_of(o + 2);
+    const T* s3 = slot_of(o + 3);
+    // magnetic potential: derivatives, then B, mu0 j, lap A right away
+    T fA[3], gA[3][3], d2A[3][3], xA[3];
+    vector_derivs<PH>(st, 1, s0, s1, s2, s3, fA, gA, d2A, xA);
+    const MagPart<T> m = mag_part<T>(gA, d2A, xA);
+    // velocity
+    T u[3], gu[3][3], d2u[3][3], xu[3];
+    vector_derivs<PH>(st, 0, s0, s1, s2, s3, u, gu, d2u, xu);
+    // log density and entropy
+    T sc[2], gsc[2][3], lap[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = h == 0 ? LNRHO : SS;
+      sc[h] = at(s0, q, 0, 0);
+      T d1a[2], d2a[2], dlx[3], dly[3], d2z;
+      axis_xy(s0, q, sc[h], d1a, d2a, dlx, dly);
+      axis_z<PH>(st, q, sc[h], at(s1, q, 0, 0), at(s2, q, 0, 0), at(s3, q, 0, 0), gsc[h][2], d2z);
+      gsc[h][0] = d1a[0];
+      gsc[h][1] = d1a[1];
+      lap[h] = (d2a[0] + d2a[1]) + d2z;
+    }
+    T rhs[NF];
+    rhs_rest<T>(sc[0], sc[1], u, gsc[0], gsc[1], gu, lap[0], lap[1], d2u, xu, m, C, rhs);
+    const T fk[NF] = {sc[0], u[0], u[1], u[2], sc[1], fA[0], fA[1], fA[2]};
+    if (active) {
+      const long long gidx = (long long)o * g.sz + (long long)y * g.sy + x;
+      if (MODE == 0) {
+        const T* pv = prevbuf + ((o & 1) * NF) * Z::PSZ + pcell;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) out.f[q][gidx] = rk_update<T>(k, fk[q], k > 0 ? pv[q * Z::PSZ] : (T)0, rhs[q], C);
+      } else {
+        const long long n = (long long)g.nx * g.ny * g.nz;
+        const long long li = ((long long)o * g.ny + y) * g.nx + x;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) rhs_out[q * n + li] = rhs[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % 3] = fk[q];
+  }
+};
+
+template <typename T, int TX, int TY, int MODE>
+__global__ void __launch_bounds__(TX* TY, 1)
+    zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C, int k,
+                  T* __restrict__ rhs_out, int nzc, int xo) {
+  using Z = ZCfg<T, TX, TY>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+  T* const ring = reinterpret_cast<T*>(base);
+  T* const prevbuf = ring + Z::NSLOT * Z::SLOT;
+  uint64_t* const mbar = reinterpret_cast<uint64_t*>(prevbuf + 2 * NF * Z::PSZ);
+
+  const int tid = (int)threadIdx.x;
+  const int tx = tid % TX, ty = tid / TX;
+  const int x0 = r.lo[0] + (int)blockIdx.x * TX, y0 = r.lo[1] + (int)blockIdx.y * TY;
+  const int zb = r.lo[2] + (int)blockIdx.z * nzc;
+  const int ze = min(zb + nzc, r.lo[2] + r.ext[2]);
+  const int x = x0 + tx, y = y0 + ty;
+  const bool active = x < r.lo[0] + r.ext[0] && y < r.lo[1] + r.ext[1];
+  const bool need_prev = MODE == 0 && k > 0;
+  const int first = zb - 3;
+  const int xs = (x0 - 3) & ~(Z::CH - 1);  // 16-byte aligned box starts (interior origin is 128-B aligned)
+  const int pxs = x0 & ~(Z::CH - 1);
+
+  if (tid == 0) {
+    for (int s = 0; s < Z::NSLOT; ++s) mbar_init(&mbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // one TMA transaction per staged plane P: its halo tile, plus f_{k-1} of output plane P - 3
+  auto issue = [&](int P) {
+    const int s = (P - first) % Z::NSLOT;
+    const int po = P - 3;
+    const bool pv = need_prev && po >= zb && po < ze;
+    mbar_expect_tx(&mbar[s], Z::HALO_TX + (pv ? Z::PREV_TX : 0u));
+    T* dst = ring + s * Z::SLOT;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) tma_load_3d(dst + q * Z::FSZ, &tm.halo[q], &mbar[s], xs + xo, y0, P + 3);
+    if (pv) {
+      T* pd = prevbuf + (po & 1) * NF * Z::PSZ;
+#pragma unroll
+      for (int q = 0; q < NF; ++q) tma_load_3d(pd + q * Z::PSZ, &tm.prev[q], &mbar[s], pxs + xo, y0 + 3, po + 3);
+    }
+  };
+  auto wait_plane = [&](int P) {
+    const int rel = P - first;
+    mbar_wait(&mbar[rel % Z::NSLOT], (unsigned)((rel / Z::NSLOT) & 1));
+  };
+
+  const ZStep<T, TX, TY, MODE> S{ring, prevbuf, C, (ty + R) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs), first};
+  March<T> st;
+#pragma unroll
+  for (int v = 0; v < 2; ++v)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
+
+  if (tid == 0)
+    for (int P = first; P <= zb; ++P) issue(P);
+  wait_plane(first);
+  wait_plane(first + 1);
+  wait_plane(first + 2);
+
+  auto iter = [&](auto ph, int p) {
+    constexpr int PH = decltype(ph)::value;
+    __syncthreads();  // every thread is done with iteration p - 1 (its slot is reused now)
+    if (tid == 0 && p + 4 <= ze + 2) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(p + 4);
+    }
+    wait_plane(p + 3);
+    if (p < zb)
+      S.template push_only<PH>(st, p);
+    else
+      S.template full<PH>(st, p, out, g, k, active, x, y, rhs_out);
+  };
+#pragma unroll 1
+  for (int p = first; p < ze; p += 3) {
+    iter(std::integral_constant<int, 0>{}, p);
+    if (p + 1 < ze) iter(std::integral_constant<int, 1>{}, p + 1);
+    if (p + 2 < ze) iter(std::integral_constant<int, 2>{}, p + 2);
+  }
+}
+
+constexpr int kNZC = 64;
+
+template <typename T, int MODE>
+void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
+                const Coef<T>& C, int k, T* rhs_out, int xo) {
+  using Z = ZCfg<T, kZTX, kZTY>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(zmarch_kernel<T, kZTX, kZTY, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM);
+    attr = true;
+  }
+  const int nzc = r.ext[2] < kNZC ? r.ext[2] : kNZC;
+  dim3 grd((r.ext[0] + kZTX - 1) / kZTX, (r.ext[1] + kZTY - 1) / kZTY, (r.ext[2] + nzc - 1) / nzc);
+  zmarch_kernel<T, kZTX, kZTY, MODE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo);
+}
+
+}  // namespace
+
 template <typename T>
-void launch_zmarch(cudaStream_t, const Fields<T>&, const Fields<T>&, const Geom&, const Region&, const Coef<T>&, int, T*) {}
+bool zmarch_supported(const Geom& g, const Region& r) {
+  (void)g;
+  return r.ext[0] >= 16 && r.ext[1] >= 4 && r.ext[2] >= 1;
+}
+
+template <typename T>
+void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
+                   const Coef<T>& C, int k, T* rhs_out, int xo) {
+  if (rhs_out)
+    launch_cfg<T, 1>(st, tm, out, g, r, C, k, rhs_out, xo);
+  else
+    launch_cfg<T, 0>(st, tm, out, g, r, C, k, nullptr, xo);
+}
+
 template bool zmarch_supported<float>(const Geom&, const Region&);
 template bool zmarch_supported<double>(const Geom&, const Region&);
-template void launch_zmarch<float>(cudaStream_t, const Fields<float>&, const Fields<float>&, const Geom&, const Region&, const Coef<float>&, int, float*);
-template void launch_zmarch<double>(cudaStream_t, const Fields<double>&, const Fields<double>&, const Geom&, const Region&, const Coef<double>&, int, double*);
+template void launch_zmarch<float>(cudaStream_t, const TmapSet&, const Fields<float>&, const Geom&, const Region&,
+                                   const Coef<float>&, int, float*, int);
+template void launch_zmarch<double>(cudaStream_t, const TmapSet&, const Fields<double>&, const Geom&, const Region&,
+                                    const Coef<double>&, int, double*, int);
+
 }  // namespace b2

@@ -1,0 +1,6 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_zm3.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_zm3.log
+timeout 600 python bench.py --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_zm3.log 2>&1
+timeout 600 python bench.py --e2e-steps 0 --no-cpu-baseline --dtype f32 > gpurun_out/bench_zm3_f32.log 2>&1
+python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/plain_zm3.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:zmarch_kernel -s 2 -c 1 -o gpurun_out/prof_zm3 python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_zm3.log 2>&1
+echo done
