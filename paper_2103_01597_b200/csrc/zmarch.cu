@@ -65,7 +65,7 @@ struct ZCfg {
   static constexpr int PSZ = (TY * PCOLS * ES + 127) / 128 * 128 / ES;  // f_{k-1} tile per field
   static constexpr unsigned HALO_TX = (unsigned)(NF * ROWS * COLS * ES);
   static constexpr unsigned PREV_TX = (unsigned)(NF * TY * PCOLS * ES);
-  static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128 + 128;
+  static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128;
 };
 
 // Register state carried along z by one thread.
@@ -262,9 +262,11 @@ __global__ void __launch_bounds__(TX* TY, 1)
     zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C, int k,
                   T* __restrict__ rhs_out, int nzc, int xo) {
   using Z = ZCfg<T, TX, TY>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
-  T* const ring = reinterpret_cast<T*>(base);
+  // Dynamic shared memory starts at the (1024-B aligned) base of the CTA window (no static
+  // shared memory in this kernel).  The pointer must stay visibly __shared__ so that the stencil
+  // reads compile to LDS, not generic loads.
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  T* const ring = reinterpret_cast<T*>(smem_raw);
   T* const prevbuf = ring + Z::NSLOT * Z::SLOT;
   uint64_t* const mbar = reinterpret_cast<uint64_t*>(prevbuf + 2 * NF * Z::PSZ);
 
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
   const int pxs = x0 & ~(Z::CH - 1);
 
   if (tid == 0) {
+    if (smem_u32(smem_raw) & 127) __trap();  // TMA destinations need 128-B alignment
     for (int s = 0; s < Z::NSLOT; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
