@@ -105,6 +105,8 @@ def peaks():
 # FP64 issue peak measured on this pool's B200 with a DFMA microbenchmark
 # (tools/microbench/fp64_peak.cu, profiles/r01_fp64_lds_microbench.txt): 17.09 T DFMA-lane/s.
 FP64_PEAK_LANE_OPS = 17.09e12
+DP_PER_CELL = 634.2          # executed DP instructions per cell-substep (ncu, zmarch_kernel<double>, k = 2)
+NF_BYTES = {"f64": 64, "f32": 32}  # 8 fields x sizeof(T)
 
 
 def cpu_baseline(n_glob, ds, params, dt, seconds_hint=True):
@@ -264,11 +266,19 @@ def main():
     hbm_peak = peaks().get("hbm_gbs", 6650.0)
     achieved_gbs = up["bytes"] / (up["ms"] * 1e-3) / 1e9 if up["ms"] > 0 else None
     local_cells = nx * ny * nz
-    # FP64 lane operations per cell-substep of the canonical per-cell arithmetic
-    dp_per_cell = float(os.environ.get("B2_DP_PER_CELL", "0")) or None
+    # FP64 lane operations per cell-substep executed by the update kernel (DFMA + DADD + DMUL,
+    # ncu source counters of zmarch_kernel<double>, profiles/r01/ncu_zmarch_*.txt)
+    dp_per_cell = DP_PER_CELL if dtype == b2.MHD_F64 else None
+    ncu = {}
+    try:
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_latest.json")))
+    except Exception:
+        pass
     substep_ms = ms_total / (3 * args.steps)
+    traffic = ncu.get("dram_bytes_per_launch") if ncu.get("dtype") == args.dtype and world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved_gbs / hbm_peak if achieved_gbs else None, "traffic": None,
+                "frac": achieved_gbs / hbm_peak if achieved_gbs else None, "traffic": traffic,
+                "traffic_note": ncu.get("note") if traffic else None,
                 "kernel": "update (fused stencil + RHS + RK3)", "avg_launch_ms": upd_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
     step_share = up["ms"] / max(ms_total, 1e-9)
@@ -317,10 +327,13 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
-        if dp_per_cell:
-            ach = dp_per_cell * local_cells * (up["launches"] / max(up["launches"], 1)) / (upd_ms * 1e-3)
+        if dp_per_cell and up["ms"] > 0:
+            upd_cells = up["bytes"] / (NF_BYTES[args.dtype] * (2 + 3 + 3) / 3)  # cells x substeps updated
+            ach = dp_per_cell * upd_cells / (up["ms"] * 1e-3)
             line["roofline_fp64"] = {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_LANE_OPS,
-                                     "unit": "DP lane-ops/s", "frac": ach / FP64_PEAK_LANE_OPS}
+                                     "unit": "DP lane-ops/s", "frac": ach / FP64_PEAK_LANE_OPS,
+                                     "dp_per_cell": dp_per_cell,
+                                     "peak_source": "measured DFMA microbenchmark (profiles/r01_fp64_lds_microbench.txt)"}
         print(json.dumps(line), flush=True)
     mesh.close()
     if dist is not None:

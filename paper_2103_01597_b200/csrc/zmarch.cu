@@ -2,10 +2,12 @@
 //
 // A CTA owns a TX x TY column of cells and marches it along z over a chunk of planes.
 //  * Staging: each plane (8 fields, tile + radius-3 halo in x and y) is fetched by TMA
-//    (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion) into a 5-slot
-//    shared-memory ring, one plane ahead of the computation; f_{k-1} of the output plane
-//    (read pointwise by the RK3 update) rides in the same transaction.  One CTA barrier per
-//    plane protects slot reuse.
+//    (cp.async.bulk.tensor.3d, mbarrier completion) into a 5-slot shared-memory ring, one plane
+//    ahead of the computation; f_{k-1} of the output plane (read pointwise by the RK3 update)
+//    rides in the same transaction.  There is no CTA barrier in the march: each warp releases a
+//    slot when it is done with it (shared-memory counter), and the last warp to release issues
+//    the TMA that refills it, so warps drift up to one plane apart instead of hitting their
+//    shared-memory-heavy and FP64-heavy phases in lockstep.
 //  * In-plane derivatives (x, y axes and the d_x d_y diagonals of Eq. 14) are read
 //    from the slot of the output plane o; the z column of every field comes from registers
 //    (planes o-3..o-1) and from the ring (o+1..o+3).
@@ -66,6 +68,7 @@ struct ZCfg {
   static constexpr unsigned HALO_TX = (unsigned)(NF * ROWS * COLS * ES);
   static constexpr unsigned PREV_TX = (unsigned)(NF * TY * PCOLS * ES);
   static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128;
+  static constexpr unsigned NWARPS = (unsigned)(NT / 32);
 };
 
 // Register state carried along z by one thread.
@@ -269,6 +272,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
   T* const ring = reinterpret_cast<T*>(smem_raw);
   T* const prevbuf = ring + Z::NSLOT * Z::SLOT;
   uint64_t* const mbar = reinterpret_cast<uint64_t*>(prevbuf + 2 * NF * Z::PSZ);
+  unsigned* const released = reinterpret_cast<unsigned*>(mbar + Z::NSLOT);  // warps done with a slot
 
   const int tid = (int)threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -284,7 +288,10 @@ __global__ void __launch_bounds__(TX* TY, 1)
 
   if (tid == 0) {
     if (smem_u32(smem_raw) & 127) __trap();  // TMA destinations need 128-B alignment
-    for (int s = 0; s < Z::NSLOT; ++s) mbar_init(&mbar[s], 1);
+    for (int s = 0; s < Z::NSLOT; ++s) {
+      mbar_init(&mbar[s], 1);
+      released[s] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -319,23 +326,31 @@ __global__ void __launch_bounds__(TX* TY, 1)
       for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
 
   if (tid == 0)
-    for (int P = first; P <= zb; ++P) issue(P);
+    for (int P = first; P <= zb + 1 && P <= ze + 2; ++P) issue(P);
   wait_plane(first);
   wait_plane(first + 1);
   wait_plane(first + 2);
 
+  const bool lane0 = (tid & 31) == 0;
   auto iter = [&](auto ph, int p) {
     constexpr int PH = decltype(ph)::value;
-    __syncthreads();  // every thread is done with iteration p - 1 (its slot is reused now)
-    if (tid == 0 && p + 4 <= ze + 2) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(p + 4);
-    }
-    wait_plane(p + 3);
+    wait_plane(p + 3);  // plane p+3 and f_{k-1}(p) have landed
     if (p < zb)
       S.template push_only<PH>(st, p);
     else
       S.template full<PH>(st, p, out, g, k, active, x, y, rhs_out);
+    // release slot(p) (and the f_{k-1} buffer of plane p); the last warp refills it with p + 5
+    __syncwarp();
+    if (lane0) {
+      const int s = (p - first) % Z::NSLOT;
+      if (atomicAdd(&released[s], 1u) == Z::NWARPS - 1) {
+        released[s] = 0;
+        if (p + 5 <= ze + 2) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          issue(p + 5);
+        }
+      }
+    }
   };
 #pragma unroll 1
   for (int p = first; p < ze; p += 3) {
