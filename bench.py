@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--corners", action="store_true")
+    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="nccl",
+                    help="N > 1: fused peer-memory boundary stores (p2p) or NCCL send/recv of packed segments")
     return ap.parse_args()
 
 
@@ -207,7 +209,7 @@ def main():
     es = 8 if dtype == b2.MHD_F64 else 4
     ds = synth.spacing(n_glob)
     mesh = b2.Mesh(n_glob, ds, synth.P0, dtype, rank=rank, nranks=world, exchange_corners=args.corners,
-                   kernel=args.kernel)
+                   kernel=args.kernel, exchange=args.exchange)
     nz, ny, nx = mesh.shape
     lo = tuple(c * n for c, n in zip(reversed(mesh.coord), (nz, ny, nx)))
     npdt = np.float64 if dtype == b2.MHD_F64 else np.float32
@@ -316,7 +318,8 @@ def main():
                        "grid": list(n_glob), "local_grid": [nx, ny, nz], "partition": list(mesh.P),
                        "substeps_per_step": 3, "dt": dt, "params": "P0",
                        "l2": "inputs larger than L2 (no flush)", "kernel": args.kernel,
-                       "exchange_corners": bool(args.corners)},
+                       "exchange_corners": bool(args.corners),
+                       "exchange": mesh.exchange},
             "ms_per_substep": substep_ms,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -131,6 +131,17 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
 mhd_status mhd_nccl_unique_id(void* out128);
 mhd_status mhd_comm_init(mhd_mesh* mesh, const void* nccl_unique_id);
 
+/* Peer-memory halo exchange over NVLink / NVSwitch (all ranks on one box).  Each rank exports
+ * its workspace as a CUDA IPC handle blob of MHD_P2P_HANDLE_BYTES; the caller all-gathers the
+ * blobs in rank order and passes them to mhd_p2p_open (collective, after every rank created its
+ * mesh; follow it with a host barrier).  From then on the outer-shell update kernels store their
+ * boundary results directly into the neighbours' halos (no pack, send/recv or unpack), ordered by
+ * system-scope flags in the workspaces.  mhd_set_exchange(mesh, 0) returns to NCCL. */
+#define MHD_P2P_HANDLE_BYTES 80
+mhd_status mhd_p2p_export(mhd_mesh* mesh, void* out_blob);
+mhd_status mhd_p2p_open(mhd_mesh* mesh, const void* blobs);
+mhd_status mhd_set_exchange(mhd_mesh* mesh, int32_t mode); /* 0: NCCL, 1: peer memory */
+
 mhd_status mhd_mesh_destroy(mhd_mesh* mesh);
 
 /* ---- state I/O ------------------------------------------------------------ */

@@ -15,13 +15,14 @@ MHD_ABI_VERSION = 1
 MHD_RADIUS = 3
 MHD_NFIELDS = 8
 MHD_F32, MHD_F64 = 4, 8
+MHD_P2P_HANDLE_BYTES = 80
 MHD_MIN, MHD_MAX, MHD_SUM, MHD_RMS, MHD_SUM_EXP = range(5)
 STATUS = {0: "MHD_OK", 1: "MHD_EINVAL", 2: "MHD_EDECOMP", 3: "MHD_ESMALL", 4: "MHD_EUNSUPPORTED",
           5: "MHD_ECUDA", 6: "MHD_ENCCL", 7: "MHD_ENOMEM", 8: "MHD_ENONFINITE", 9: "MHD_ESTATE"}
 
 # every symbol include/b2mhd.h declares
 SYMBOLS = ("mhd_decompose", "mhd_segment_table", "mhd_workspace_bytes", "mhd_mesh_create", "mhd_nccl_unique_id",
-           "mhd_comm_init", "mhd_mesh_destroy", "mhd_load", "mhd_store", "mhd_store_grid", "mhd_halo_exchange",
+           "mhd_comm_init", "mhd_p2p_export", "mhd_p2p_open", "mhd_set_exchange", "mhd_mesh_destroy", "mhd_load", "mhd_store", "mhd_store_grid", "mhd_halo_exchange",
            "mhd_integrate_substep", "mhd_integrate_step", "mhd_reduce", "mhd_debug_rhs", "mhd_synchronize",
            "mhd_set_kernel", "mhd_mesh_query", "mhd_launch_count", "mhd_profile_enable", "mhd_profile_read", "mhd_status_str", "mhd_last_error",
            "mhd_abi_version")
@@ -63,6 +64,9 @@ def _load():
         "mhd_nccl_unique_id": [ctypes.c_void_p],
         "mhd_comm_init": [ctypes.c_void_p, ctypes.c_void_p],
         "mhd_mesh_destroy": [ctypes.c_void_p],
+        "mhd_p2p_export": [ctypes.c_void_p, ctypes.c_void_p],
+        "mhd_p2p_open": [ctypes.c_void_p, ctypes.c_void_p],
+        "mhd_set_exchange": [ctypes.c_void_p, ctypes.c_int32],
         "mhd_load": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32],
         "mhd_store": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32],
         "mhd_store_grid": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32],
@@ -161,6 +165,22 @@ def mhd_nccl_unique_id() -> bytes:
 def mhd_comm_init(mesh: int, uid: bytes) -> None:
     buf = ctypes.create_string_buffer(bytes(uid), 128)
     check(lib.mhd_comm_init(ctypes.c_void_p(mesh), buf), "mhd_comm_init")
+
+
+def mhd_p2p_export(mesh: int) -> bytes:
+    buf = ctypes.create_string_buffer(MHD_P2P_HANDLE_BYTES)
+    check(lib.mhd_p2p_export(ctypes.c_void_p(mesh), buf), "mhd_p2p_export")
+    return buf.raw
+
+
+def mhd_p2p_open(mesh: int, blobs) -> None:
+    raw = b"".join(bytes(b) for b in blobs)
+    buf = ctypes.create_string_buffer(raw, len(raw))
+    check(lib.mhd_p2p_open(ctypes.c_void_p(mesh), buf), "mhd_p2p_open")
+
+
+def mhd_set_exchange(mesh: int, mode: int) -> None:
+    check(lib.mhd_set_exchange(ctypes.c_void_p(mesh), mode), "mhd_set_exchange")
 
 
 def mhd_mesh_destroy(mesh: int) -> None:

@@ -21,9 +21,10 @@ struct GAcc {
 };
 
 // MODE 0: RK3 update into `out` (which holds f_{k-1} for k > 0); MODE 1: RHS to rhs_out.
-template <typename T, int MODE>
+// REMOTE: also deliver the new boundary values into the neighbours' halos (remote.cuh).
+template <typename T, int MODE, bool REMOTE>
 __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out, Geom g, Region r, Coef<T> C,
-                                                     int k, T* __restrict__ rhs_out) {
+                                                     int k, T* __restrict__ rhs_out, RemoteMap<T> rm) {
   const int x = r.lo[0] + blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r.lo[1] + blockIdx.y * blockDim.y + threadIdx.y;
   const int z = r.lo[2] + blockIdx.z * blockDim.z + threadIdx.z;
@@ -35,10 +36,16 @@ __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out
   T rhs[NF];
   rhs_cell<T>(D, C, rhs);
   if (MODE == 0) {
+    T fn[NF];
 #pragma unroll
     for (int q = 0; q < NF; ++q) {
       const T fprev = k > 0 ? out.f[q][base] : (T)0;
-      out.f[q][base] = rk_update<T>(k, D.f[q], fprev, rhs[q], C);
+      fn[q] = rk_update<T>(k, D.f[q], fprev, rhs[q], C);
+      out.f[q][base] = fn[q];
+    }
+    if (REMOTE) {
+      remote_store<T>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, z, fn);
+      __threadfence_system();
     }
   } else {
     const long long n = (long long)g.nx * g.ny * g.nz;
@@ -50,15 +57,76 @@ __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out
 
 template <typename T>
 void launch_direct(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out) {
+                   const Coef<T>& C, int k, T* rhs_out, const RemoteMap<T>* rm) {
   if (r.ext[0] <= 0 || r.ext[1] <= 0 || r.ext[2] <= 0) return;
   // thin x-slabs of the outer shell get a block shaped along y
   const dim3 blk = r.ext[0] >= 16 ? dim3(32, 4, 1) : dim3(r.ext[0], (128 / r.ext[0]) < 32 ? (128 / r.ext[0]) : 32, 1);
   dim3 grd((r.ext[0] + blk.x - 1) / blk.x, (r.ext[1] + blk.y - 1) / blk.y, (r.ext[2] + blk.z - 1) / blk.z);
+  RemoteMap<T> none;
   if (rhs_out)
-    direct_kernel<T, 1><<<grd, blk, 0, st>>>(in, out, g, r, C, k, rhs_out);
+    direct_kernel<T, 1, false><<<grd, blk, 0, st>>>(in, out, g, r, C, k, rhs_out, none);
+  else if (rm)
+    direct_kernel<T, 0, true><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr, *rm);
   else
-    direct_kernel<T, 0><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr);
+    direct_kernel<T, 0, false><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr, none);
+}
+
+// ---- peer-memory exchange helpers -------------------------------------------------------------------
+// Copy of the remote segments of a state (SegDesc::buf_off = peer slot) straight into the peers'
+// halos of the same state: the halo exchange of a freshly loaded state.
+template <typename T>
+__global__ void __launch_bounds__(256) remote_copy_kernel(Fields<T> F, Geom g, SegList L, RemoteMap<T> rm) {
+  int s = 0;
+  while (s + 1 < L.n && (int)blockIdx.x >= L.s[s + 1].block0) ++s;
+  const SegDesc& d = L.s[s];
+  const long long c = (long long)(blockIdx.x - d.block0) * blockDim.x + threadIdx.x;
+  if (c < d.count) {
+    const int cx = (int)(c % d.ext[0]);
+    const long long rr = c / d.ext[0];
+    const int cy = (int)(rr % d.ext[1]);
+    const int cz = (int)(rr / d.ext[1]);
+    const long long so = (long long)(d.src[2] + cz) * g.sz + (long long)(d.src[1] + cy) * g.sy + (d.src[0] + cx);
+    const long long dof = (long long)(d.dst[2] + cz) * g.sz + (long long)(d.dst[1] + cy) * g.sy + (d.dst[0] + cx);
+    const int p = (int)d.buf_off;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) rm.f[p][q][dof] = F.f[q][so];
+  }
+  __threadfence_system();
+}
+
+template <typename T>
+void launch_remote_copy(cudaStream_t st, const Fields<T>& fl, const Geom& g, const SegList& L, const RemoteMap<T>& rm) {
+  if (L.n == 0 || L.nblocks == 0) return;
+  remote_copy_kernel<T><<<L.nblocks, 256, 0, st>>>(fl, g, L, rm);
+}
+
+// Cross-GPU ordering with system-scope flags: after an operation that writes into the peers' halos
+// (or reads the local halo), each rank publishes its operation count into every neighbour's flag
+// slot; before the next such operation it waits until all neighbours published the previous count.
+__global__ void p2p_signal_kernel(FlagSet fs, unsigned long long seq) {
+  __threadfence_system();
+  for (int i = 0; i < fs.n; ++i)
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(fs.ptr[i]), "l"(seq) : "memory");
+}
+
+__global__ void p2p_wait_kernel(FlagSet fs, unsigned long long seq) {
+  for (int i = 0; i < fs.n; ++i) {
+    const long long t0 = clock64();
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(fs.ptr[i]) : "memory");
+      if (v >= seq) break;
+      __nanosleep(128);
+      if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: a neighbour never arrived
+    }
+  }
+}
+
+void launch_p2p_signal(cudaStream_t st, const FlagSet& fs, unsigned long long seq) {
+  p2p_signal_kernel<<<1, 1, 0, st>>>(fs, seq);
+}
+void launch_p2p_wait(cudaStream_t st, const FlagSet& fs, unsigned long long seq) {
+  p2p_wait_kernel<<<1, 1, 0, st>>>(fs, seq);
 }
 
 // ---- halo segments ---------------------------------------------------------
@@ -184,7 +252,9 @@ void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scra
 // ---- explicit instantiations ----------------------------------------------------------------------
 #define B2_INST(T)                                                                                       \
   template void launch_direct<T>(cudaStream_t, const Fields<T>&, const Fields<T>&, const Geom&,           \
-                                 const Region&, const Coef<T>&, int, T*);                                 \
+                                 const Region&, const Coef<T>&, int, T*, const RemoteMap<T>*);            \
+  template void launch_remote_copy<T>(cudaStream_t, const Fields<T>&, const Geom&, const SegList&,        \
+                                      const RemoteMap<T>&);                                              \
   template void launch_segments<T>(cudaStream_t, const Fields<T>&, const Geom&, const SegList&, int, T*); \
   template void launch_reduce<T>(cudaStream_t, const T*, const Geom&, double*, int);
 B2_INST(float)

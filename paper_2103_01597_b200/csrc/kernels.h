@@ -7,6 +7,7 @@
 #include <type_traits>
 
 #include "mhd_math.cuh"
+#include "remote.cuh"
 
 namespace b2 {
 
@@ -47,7 +48,16 @@ struct Region {
 // ---- launchers (kernels.cu) ----
 template <typename T>
 void launch_direct(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, const Geom& g,
-                   const Region& r, const Coef<T>& C, int k, T* rhs_out);
+                   const Region& r, const Coef<T>& C, int k, T* rhs_out, const RemoteMap<T>* rm = nullptr);
+// peer-memory exchange: copy the remote segments of a state into the peers' halos; flags
+template <typename T>
+void launch_remote_copy(cudaStream_t st, const Fields<T>& fl, const Geom& g, const SegList& L, const RemoteMap<T>& rm);
+struct FlagSet {
+  unsigned long long* ptr[kMaxPeers];
+  int n;
+};
+void launch_p2p_signal(cudaStream_t st, const FlagSet& fs, unsigned long long seq);
+void launch_p2p_wait(cudaStream_t st, const FlagSet& fs, unsigned long long seq);
 template <typename T>
 void launch_segments(cudaStream_t st, const Fields<T>& fl, const Geom& g, const SegList& L, int kind, T* buf);
 template <typename TS, typename TD>
@@ -78,7 +88,7 @@ template <typename T>
 bool zmarch_supported(const Geom& g, const Region& r);
 template <typename T>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo);
+                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm = nullptr);
 
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 constexpr int kReduceVals = 5;      // min, max, sum, sum of squares, sum of exp

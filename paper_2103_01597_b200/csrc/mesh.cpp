@@ -200,7 +200,7 @@ struct Layout {
   int64_t n[3];
   int64_t xo;    // elements of left pad: interior x = 0 sits at row offset xo (128-byte aligned)
   int64_t sy, sz, field_elems, origin;
-  size_t field_bytes, state_off[2], send_off, recv_off, red_off, total;
+  size_t field_bytes, state_off[2], send_off, recv_off, red_off, flags_off, total;
   int64_t send_cells, recv_cells;
 };
 
@@ -237,6 +237,8 @@ Layout make_layout(const mhd_mesh_info* info, int rank, const std::vector<SegInf
   off = align_up(off + (size_t)L.recv_cells * NF * es, 256);
   L.red_off = off;
   off = align_up(off + kReduceBlocks * kReduceVals * sizeof(double), 256);
+  L.flags_off = off;  // peer-memory exchange: one operation counter per rank, written by that rank
+  off = align_up(off + (size_t)info->nranks * sizeof(unsigned long long), 256);
   L.total = off;
   return L;
 }
@@ -268,6 +270,31 @@ struct mhd_mesh {
   double* h_red = nullptr;  // pinned
   TmapSet tmaps[2];          // [state read with the stencil]
   bool tmaps_ok = false;
+  // peer-memory (NVLink) exchange
+  int exchange = 0;                 // 0: NCCL send/recv of packed segments; 1: fused peer-memory stores
+  std::vector<char*> peer_ws;       // workspace of every rank as mapped here (nullptr: not a neighbour)
+  std::vector<void*> ipc_bases;     // opened IPC allocations (closed at destroy)
+  unsigned long long seq = 0;       // operations that touched halos across ranks
+  bool halo_valid = false;          // halos of the current state already delivered by the last update
+  SegList remote_list;              // remote segments with buf_off = peer slot (halo copy after a load)
+  FlagSet sig, wt;
+  template <typename T>
+  RemoteMap<T> remote_map(int dest_state) const {
+    RemoteMap<T> rm;
+    memset(&rm, 0, sizeof(rm));
+    for (int c = 0; c < 27; ++c) rm.peer_of[c] = -1;
+    for (size_t i = 0; i < peers.size() && i < (size_t)kMaxPeers; ++i)
+      for (int q = 0; q < NF; ++q)
+        rm.f[i][q] = reinterpret_cast<T*>(peer_ws[peers[i].peer] + L.state_off[dest_state] + (size_t)q * L.field_bytes) +
+                     L.origin;
+    for (auto& si : segs) {
+      if (si.self) continue;
+      const int code = (si.s.offset[0] + 1) + 3 * (si.s.offset[1] + 1) + 9 * (si.s.offset[2] + 1);
+      for (size_t i = 0; i < peers.size(); ++i)
+        if (peers[i].peer == si.s.send_peer) rm.peer_of[code] = (signed char)i;
+    }
+    return rm;
+  }
   // profiling: (start, stop) event pairs per phase, with the algorithmic bytes of the launch
   struct Rec {
     cudaEvent_t a, b;
@@ -398,16 +425,16 @@ double seg_bytes(const SegList& L, size_t es) {
 
 // The update of one region of the subdomain.
 template <typename T>
-void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out) {
+void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out, const RemoteMap<T>* rm = nullptr) {
   const Fields<T> in = m->fields<T>(m->cur), out = m->fields<T>(1 - m->cur);
   const Coef<T> C = make_coef<T>(m->info, k, dt);
   const bool zm = m->variant != 1 && m->tmaps_ok && zmarch_supported<T>(m->g, r);
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
   PhaseTimer t(m, m->stream, MHD_PHASE_UPDATE, cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
   if (zm)
-    launch_zmarch<T>(m->stream, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo);
+    launch_zmarch<T>(m->stream, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, rm);
   else
-    launch_direct<T>(m->stream, in, out, m->g, r, C, k, rhs_out);
+    launch_direct<T>(m->stream, in, out, m->g, r, C, k, rhs_out, rm);
   m->launches++;
 }
 
@@ -483,8 +510,50 @@ void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer)
   }
 }
 
+// Peer-memory exchange.  Per substep: wait until every neighbour finished its
+// previous cross-rank operation; update the outer shell, storing boundary results locally and into
+// the neighbours' halos; publish; then update the inner segment (which needs no remote halo) while
+// the neighbours proceed.
+template <typename T>
+void p2p_halo_copy(mhd_mesh* m) {
+  launch_p2p_wait(m->stream, m->wt, m->seq);
+  const RemoteMap<T> rm = m->remote_map<T>(m->cur);
+  launch_remote_copy<T>(m->stream, m->fields<T>(m->cur), m->g, m->remote_list, rm);
+  launch_p2p_signal(m->stream, m->sig, ++m->seq);
+  m->launches += 3;
+  m->halo_valid = true;
+}
+
+template <typename T>
+mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
+  const Fields<T> F = m->fields<T>(m->cur);
+  if (m->self_list.n) {
+    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
+    launch_segments<T>(m->stream, F, m->g, m->self_list, SEG_SELF, nullptr);
+    m->launches++;
+  }
+  if (!m->halo_valid) p2p_halo_copy<T>(m);
+  Region inner;
+  std::vector<Region> outer;
+  split_regions(m, inner, outer);
+  {
+    PhaseTimer t(m, m->stream, MHD_PHASE_EXCHANGE, 0.0);
+    launch_p2p_wait(m->stream, m->wt, m->seq);
+    m->launches++;
+  }
+  const RemoteMap<T> rm = m->remote_map<T>(1 - m->cur);
+  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, rhs_out ? nullptr : &rm);
+  launch_p2p_signal(m->stream, m->sig, ++m->seq);
+  m->launches++;
+  update_region<T>(m, inner, k, dt, rhs_out);
+  if (!rhs_out) m->halo_valid = true;  // the neighbours are delivering the new state's halo
+  CU(cudaGetLastError());
+  return MHD_OK;
+}
+
 template <typename T>
 mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
+  if (m->exchange == 1) return substep_p2p<T>(m, k, dt, rhs_out);
   mhd_status st = halo_begin<T>(m);
   if (st != MHD_OK) return st;
   Region inner;
@@ -715,6 +784,7 @@ mhd_status mhd_mesh_destroy(mhd_mesh* m) {
   if (!m) return MHD_OK;
   cudaStreamSynchronize(m->stream);
   if (m->comm) ncclCommDestroy(m->comm);
+  for (void* b : m->ipc_bases) cudaIpcCloseMemHandle(b);
   if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
   if (m->ev_ready) cudaEventDestroy(m->ev_ready);
   if (m->ev_halo) cudaEventDestroy(m->ev_halo);
@@ -734,6 +804,7 @@ mhd_status mhd_load(mhd_mesh* m, int32_t field, const void* src, int32_t src_dty
   if (!m || !src || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad load argument");
   if (src_dtype != MHD_F32 && src_dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "src dtype");
   m->next_k = 0;
+  m->halo_valid = false;
   return m->info.dtype == MHD_F64 ? load_impl<double>(m, field, src, src_dtype, on_device)
                                   : load_impl<float>(m, field, src, src_dtype, on_device);
 }
@@ -760,6 +831,19 @@ mhd_status mhd_store_grid(mhd_mesh* m, int32_t field, void* dst, int32_t on_devi
 
 mhd_status mhd_halo_exchange(mhd_mesh* m) {
   if (!m) return fail(MHD_EINVAL, "null mesh");
+  if (m->exchange == 1) {
+    if (m->info.dtype == MHD_F64) {
+      launch_segments<double>(m->stream, m->fields<double>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
+      p2p_halo_copy<double>(m);
+    } else {
+      launch_segments<float>(m->stream, m->fields<float>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
+      p2p_halo_copy<float>(m);
+    }
+    launch_p2p_wait(m->stream, m->wt, m->seq);  // the neighbours' copies into this halo have landed
+    m->launches += 2;
+    CU(cudaGetLastError());
+    return MHD_OK;
+  }
   mhd_status st = m->info.dtype == MHD_F64 ? halo_begin<double>(m) : halo_begin<float>(m);
   if (st != MHD_OK) return st;
   st = m->info.dtype == MHD_F64 ? halo_end<double>(m) : halo_end<float>(m);
@@ -854,6 +938,91 @@ mhd_status mhd_mesh_query(const mhd_mesh* m, int32_t P[3], int32_t coord[3], int
     if (local_n) local_n[a] = m->L.n[a];
   }
   if (next_k) *next_k = m->next_k;
+  return MHD_OK;
+}
+
+mhd_status mhd_p2p_export(mhd_mesh* m, void* out_blob) {
+  if (!m || !out_blob) return fail(MHD_EINVAL, "null argument");
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  if (!range) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CU(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return fail(MHD_ECUDA, "cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)m->ws) != CUDA_SUCCESS) return fail(MHD_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, (void*)base));
+  unsigned char* b = static_cast<unsigned char*>(out_blob);
+  memset(b, 0, MHD_P2P_HANDLE_BYTES);
+  memcpy(b, &h, sizeof(h));
+  const uint64_t off = (uint64_t)((char*)m->ws - (char*)base);
+  memcpy(b + 64, &off, 8);
+  const int32_t rank = m->info.rank;
+  memcpy(b + 72, &rank, 4);
+  return MHD_OK;
+}
+
+mhd_status mhd_p2p_open(mhd_mesh* m, const void* blobs) {
+  if (!m || !blobs) return fail(MHD_EINVAL, "null argument");
+  if (m->info.nranks == 1) return MHD_OK;
+  if (m->peers.size() > (size_t)kMaxPeers) return fail(MHD_EUNSUPPORTED, "more than 7 neighbours");
+  CU(cudaStreamSynchronize(m->stream));  // the zeroed flags are in place before anyone signals
+  m->peer_ws.assign(m->info.nranks, nullptr);
+  const unsigned char* b = static_cast<const unsigned char*>(blobs);
+  for (auto& p : m->peers) {
+    const unsigned char* blob = b + (size_t)p.peer * MHD_P2P_HANDLE_BYTES;
+    int32_t r;
+    memcpy(&r, blob + 72, 4);
+    if (r != p.peer) return fail(MHD_EINVAL, "handle blobs are not in rank order");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, blob, sizeof(h));
+    uint64_t off;
+    memcpy(&off, blob + 64, 8);
+    void* base = nullptr;
+    CU(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    m->ipc_bases.push_back(base);
+    m->peer_ws[p.peer] = static_cast<char*>(base) + off;
+  }
+  memset(&m->sig, 0, sizeof(m->sig));
+  memset(&m->wt, 0, sizeof(m->wt));
+  for (auto& p : m->peers) {
+    m->sig.ptr[m->sig.n++] =
+        reinterpret_cast<unsigned long long*>(m->peer_ws[p.peer] + m->L.flags_off) + m->info.rank;
+    m->wt.ptr[m->wt.n++] = reinterpret_cast<unsigned long long*>(m->ws + m->L.flags_off) + p.peer;
+  }
+  // remote segments (buf_off = peer slot) for the halo copy of a freshly loaded state
+  memset(&m->remote_list, 0, sizeof(m->remote_list));
+  int nb = 0;
+  for (auto& si : m->segs) {
+    if (si.self) continue;
+    SegDesc& d = m->remote_list.s[m->remote_list.n++];
+    for (int a = 0; a < 3; ++a) {
+      d.src[a] = si.s.src_first[a];
+      d.dst[a] = si.s.dst_first[a];
+      d.ext[a] = si.s.extent[a];
+    }
+    d.count = (long long)d.ext[0] * d.ext[1] * d.ext[2];
+    for (size_t i = 0; i < m->peers.size(); ++i)
+      if (m->peers[i].peer == si.s.send_peer) d.buf_off = (long long)i;
+    d.block0 = nb;
+    nb += (int)((d.count + 255) / 256);
+  }
+  m->remote_list.nblocks = nb;
+  m->exchange = 1;
+  m->halo_valid = false;
+  return MHD_OK;
+}
+
+mhd_status mhd_set_exchange(mhd_mesh* m, int32_t mode) {
+  if (!m || mode < 0 || mode > 1) return fail(MHD_EINVAL, "mode must be 0 (NCCL) or 1 (peer memory)");
+  if (mode == 1 && m->info.nranks > 1 && m->peer_ws.empty()) return fail(MHD_EINVAL, "mhd_p2p_open first");
+  if (mode == 0 && m->info.nranks > 1 && !m->comm) return fail(MHD_ENCCL, "mhd_comm_init first");
+  m->exchange = m->info.nranks > 1 ? mode : 0;
+  m->halo_valid = false;
   return MHD_OK;
 }
 

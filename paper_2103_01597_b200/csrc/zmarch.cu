@@ -60,7 +60,10 @@ struct ZCfg {
   static constexpr int ROWS = TY + 6;
   static constexpr int FSZ = (ROWS * COLS * ES + 127) / 128 * 128 / ES;  // 128-B aligned TMA destinations
   static constexpr int SLOT = NF * FSZ;
-  static constexpr int NSLOT = 5;
+  // FP64: 5 slots (one plane of prefetch), 1 CTA/SM.  FP32: 4 slots and 2 CTAs/SM, the other CTA
+  // covering the refill latency.
+  static constexpr int NSLOT = sizeof(T) == 8 ? 5 : 4;
+  static constexpr int MINB = sizeof(T) == 8 ? 1 : 2;
   static constexpr int NT = TX * TY;
   static constexpr int CH = zm_ch<T>();
   static constexpr int PCOLS = zm_pcols<T>();
@@ -78,7 +81,7 @@ struct March {
   T acc[2][3][3];  // [u|A][logical output o, o+1, o+2 -> physical (j + PH) % 3][z-part of x_0, x_1, x_2]
 };
 
-template <typename T, int TX, int TY, int MODE>
+template <typename T, int TX, int TY, int MODE, bool REMOTE>
 struct ZStep {
   using Z = ZCfg<T, TX, TY>;
   const T* ring;
@@ -87,6 +90,7 @@ struct ZStep {
   int cell;   // offset of this thread's cell inside a field of a slot
   int pcell;  // offset inside a field of the f_{k-1} tile
   int slot0;  // plane zb - 3 (first staged plane) has slot 0
+  const RemoteMap<T>& rm;
 
   __device__ __forceinline__ const T* slot_of(int plane) const {
     return ring + ((plane - slot0) % Z::NSLOT) * Z::SLOT + cell;
@@ -246,8 +250,13 @@ struct ZStep {
       const long long gidx = (long long)o * g.sz + (long long)y * g.sy + x;
       if (MODE == 0) {
         const T* pv = prevbuf + ((o & 1) * NF) * Z::PSZ + pcell;
+        T fn[NF];
 #pragma unroll
-        for (int q = 0; q < NF; ++q) out.f[q][gidx] = rk_update<T>(k, fk[q], k > 0 ? pv[q * Z::PSZ] : (T)0, rhs[q], C);
+        for (int q = 0; q < NF; ++q) {
+          fn[q] = rk_update<T>(k, fk[q], k > 0 ? pv[q * Z::PSZ] : (T)0, rhs[q], C);
+          out.f[q][gidx] = fn[q];
+        }
+        if (REMOTE) remote_store<T>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, o, fn);
       } else {
         const long long n = (long long)g.nx * g.ny * g.nz;
         const long long li = ((long long)o * g.ny + y) * g.nx + x;
@@ -260,10 +269,10 @@ struct ZStep {
   }
 };
 
-template <typename T, int TX, int TY, int MODE>
-__global__ void __launch_bounds__(TX* TY, 1)
+template <typename T, int TX, int TY, int MODE, bool REMOTE>
+__global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
     zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C, int k,
-                  T* __restrict__ rhs_out, int nzc, int xo) {
+                  T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm) {
   using Z = ZCfg<T, TX, TY>;
   // Dynamic shared memory starts at the (1024-B aligned) base of the CTA window (no static
   // shared memory in this kernel).  The pointer must stay visibly __shared__ so that the stencil
@@ -316,7 +325,8 @@ __global__ void __launch_bounds__(TX* TY, 1)
     mbar_wait(&mbar[rel % Z::NSLOT], (unsigned)((rel / Z::NSLOT) & 1));
   };
 
-  const ZStep<T, TX, TY, MODE> S{ring, prevbuf, C, (ty + R) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs), first};
+  const ZStep<T, TX, TY, MODE, REMOTE> S{ring, prevbuf, C, (ty + R) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
+                                         first, rm};
   March<T> st;
 #pragma unroll
   for (int v = 0; v < 2; ++v)
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__(TX* TY, 1)
       for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
 
   if (tid == 0)
-    for (int P = first; P <= zb + 1 && P <= ze + 2; ++P) issue(P);
+    for (int P = first; P < first + Z::NSLOT && P <= ze + 2; ++P) issue(P);
   wait_plane(first);
   wait_plane(first + 1);
   wait_plane(first + 2);
@@ -339,15 +349,15 @@ __global__ void __launch_bounds__(TX* TY, 1)
       S.template push_only<PH>(st, p);
     else
       S.template full<PH>(st, p, out, g, k, active, x, y, rhs_out);
-    // release slot(p) (and the f_{k-1} buffer of plane p); the last warp refills it with p + 5
+    // release slot(p) (and the f_{k-1} buffer of plane p); the last warp refills it with p + NSLOT
     __syncwarp();
     if (lane0) {
       const int s = (p - first) % Z::NSLOT;
       if (atomicAdd(&released[s], 1u) == Z::NWARPS - 1) {
         released[s] = 0;
-        if (p + 5 <= ze + 2) {
+        if (p + Z::NSLOT <= ze + 2) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          issue(p + 5);
+          issue(p + Z::NSLOT);
         }
       }
     }
@@ -358,22 +368,24 @@ __global__ void __launch_bounds__(TX* TY, 1)
     if (p + 1 < ze) iter(std::integral_constant<int, 1>{}, p + 1);
     if (p + 2 < ze) iter(std::integral_constant<int, 2>{}, p + 2);
   }
+  if (REMOTE) __threadfence_system();  // peer halo stores visible before the completion signal
 }
 
 constexpr int kNZC = 64;
 
-template <typename T, int MODE>
+template <typename T, int MODE, bool REMOTE>
 void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                const Coef<T>& C, int k, T* rhs_out, int xo) {
+                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm) {
   using Z = ZCfg<T, kZTX, kZTY>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(zmarch_kernel<T, kZTX, kZTY, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM);
+    cudaFuncSetAttribute(zmarch_kernel<T, kZTX, kZTY, MODE, REMOTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Z::SMEM);
     attr = true;
   }
   const int nzc = r.ext[2] < kNZC ? r.ext[2] : kNZC;
   dim3 grd((r.ext[0] + kZTX - 1) / kZTX, (r.ext[1] + kZTY - 1) / kZTY, (r.ext[2] + nzc - 1) / nzc);
-  zmarch_kernel<T, kZTX, kZTY, MODE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo);
+  zmarch_kernel<T, kZTX, kZTY, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm);
 }
 
 }  // namespace
@@ -386,18 +398,21 @@ bool zmarch_supported(const Geom& g, const Region& r) {
 
 template <typename T>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo) {
+                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm) {
+  RemoteMap<T> none;
   if (rhs_out)
-    launch_cfg<T, 1>(st, tm, out, g, r, C, k, rhs_out, xo);
+    launch_cfg<T, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none);
+  else if (rm)
+    launch_cfg<T, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm);
   else
-    launch_cfg<T, 0>(st, tm, out, g, r, C, k, nullptr, xo);
+    launch_cfg<T, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none);
 }
 
 template bool zmarch_supported<float>(const Geom&, const Region&);
 template bool zmarch_supported<double>(const Geom&, const Region&);
 template void launch_zmarch<float>(cudaStream_t, const TmapSet&, const Fields<float>&, const Geom&, const Region&,
-                                   const Coef<float>&, int, float*, int);
+                                   const Coef<float>&, int, float*, int, const RemoteMap<float>*);
 template void launch_zmarch<double>(cudaStream_t, const TmapSet&, const Fields<double>&, const Geom&, const Region&,
-                                    const Coef<double>&, int, double*, int);
+                                    const Coef<double>&, int, double*, int, const RemoteMap<double>*);
 
 }  // namespace b2

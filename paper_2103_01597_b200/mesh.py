@@ -15,7 +15,10 @@ _TORCH_DT = {native.MHD_F64: "float64", native.MHD_F32: "float32"}
 
 class Mesh:
     def __init__(self, n_xyz, ds_xyz, params: dict, dtype: int = native.MHD_F64, rank: int = 0, nranks: int = 1,
-                 exchange_corners: bool = False, stream=None, process_group=None, kernel: int = 0):
+                 exchange_corners: bool = False, stream=None, process_group=None, kernel: int = 0,
+                 exchange: str = "nccl"):
+        """exchange (nranks > 1): "p2p" = boundary results stored straight into the neighbours' halos
+        over NVLink (CUDA IPC peer memory); "nccl" = pack, NCCL send/recv, unpack."""
         import torch
 
         if not torch.cuda.is_available():
@@ -36,7 +39,15 @@ class Mesh:
             import torch.distributed as dist
             obj = [native.mhd_nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0, group=process_group)
-            native.mhd_comm_init(self.handle, obj[0])
+            native.mhd_comm_init(self.handle, obj[0])  # reductions (and the "nccl" exchange)
+            if exchange == "p2p":
+                blobs = [None] * nranks
+                dist.all_gather_object(blobs, native.mhd_p2p_export(self.handle), group=process_group)
+                native.mhd_p2p_open(self.handle, blobs)
+                dist.barrier(group=process_group)
+            elif exchange != "nccl":
+                raise ValueError(f"exchange must be 'p2p' or 'nccl', not {exchange!r}")
+        self.exchange = exchange if nranks > 1 else "local"
         if kernel:
             native.mhd_set_kernel(self.handle, kernel)
 
@@ -100,6 +111,10 @@ class Mesh:
         native.mhd_debug_rhs(self.handle, out.data_ptr())
         self.torch.cuda.current_stream(self.device).wait_stream(self.stream)
         return out
+
+    def set_exchange(self, mode: str) -> None:
+        native.mhd_set_exchange(self.handle, {"nccl": 0, "p2p": 1}[mode])
+        self.exchange = mode
 
     def set_kernel(self, variant: int) -> None:
         native.mhd_set_kernel(self.handle, variant)

@@ -15,8 +15,9 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _run(nproc, N, corners=0, steps=3, port=29511):
-    env = dict(os.environ, MGPU_N=",".join(map(str, N)), MGPU_CORNERS=str(corners), MGPU_STEPS=str(steps))
+def _run(nproc, N, corners=0, steps=3, port=29511, exchange="p2p"):
+    env = dict(os.environ, MGPU_N=",".join(map(str, N)), MGPU_CORNERS=str(corners), MGPU_STEPS=str(steps),
+               MGPU_EXCHANGE=exchange)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tools", "mgpu_check.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
@@ -25,9 +26,11 @@ def _run(nproc, N, corners=0, steps=3, port=29511):
 
 @pytest.mark.parametrize("nproc", [2, 4, 8])
 @pytest.mark.parametrize("corners", [0, 1])
-def test_multigpu_halo_and_bit_identity(nproc, corners):
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_multigpu_halo_and_bit_identity(nproc, corners, exchange):
+    """Both exchanges give the 1-GPU result bit for bit (so they agree with each other)."""
     if _ngpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     N = {2: (40, 36, 32), 4: (40, 32, 32), 8: (32, 32, 32)}[nproc]
-    rc, out = _run(nproc, N, corners, port=29500 + nproc * 2 + corners)
+    rc, out = _run(nproc, N, corners, port=29500 + nproc * 4 + corners * 2 + (exchange == "p2p"), exchange=exchange)
     assert rc == 0, out[-4000:]

@@ -34,11 +34,14 @@ def main():
     N = tuple(int(v) for v in os.environ.get("MGPU_N", "48,40,32").split(","))  # (x, y, z)
     steps = int(os.environ.get("MGPU_STEPS", "3"))
     corners = bool(int(os.environ.get("MGPU_CORNERS", "0")))
+    exchange = os.environ.get("MGPU_EXCHANGE", "p2p")
     ds = synth.spacing(N)
     res = {"rank": rank, "world": world, "N": N}
     ok = True
 
-    mesh = b2.Mesh(N, ds, synth.P0, b2.MHD_F64, rank=rank, nranks=world, exchange_corners=corners)
+    mesh = b2.Mesh(N, ds, synth.P0, b2.MHD_F64, rank=rank, nranks=world, exchange_corners=corners,
+                   exchange=exchange)
+    res["exchange"] = exchange
     Pz = tuple(reversed(mesh.P))
     cz = tuple(reversed(mesh.coord))
     res["P_xyz"], res["coord_xyz"] = mesh.P, mesh.coord
