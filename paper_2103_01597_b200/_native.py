@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libb2mhd.so")
+LIB_PATH = os.environ.get("B2MHD_LIB") or os.path.join(HERE, "libb2mhd.so")
 
 MHD_ABI_VERSION = 1
 MHD_RADIUS = 3

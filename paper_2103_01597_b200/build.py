@@ -10,6 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libb2mhd.so")
+# Experimental variants (e.g. B2_ZM_TX64=16) build to libb2mhd_<tag>.so; load with B2MHD_LIB=<path>.
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -40,14 +41,17 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=None, lib=None) -> str:
+    global LIB
+    if lib:
+        LIB = lib
     if not force and up_to_date():
         return LIB
     inc, lib = nccl_dirs()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + ("_" + "_".join(defines) if defines else ""))
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-I", inc, "-I", INCLUDE,
-              "--expt-relaxed-constexpr"] + ARCH
+              "--expt-relaxed-constexpr"] + ARCH + ["-D" + d for d in (defines or [])]
     objs = []
     procs = []
     for src in sources():
@@ -71,4 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    tag = "_".join(d.replace("=", "") for d in defs)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs or None,
+                lib=os.path.join(HERE, f"libb2mhd_{tag}.so") if defs else None))

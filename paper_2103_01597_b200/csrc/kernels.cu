@@ -79,12 +79,14 @@ __global__ void __launch_bounds__(256) remote_copy_kernel(Fields<T> F, Geom g, S
   int s = 0;
   while (s + 1 < L.n && (int)blockIdx.x >= L.s[s + 1].block0) ++s;
   const SegDesc& d = L.s[s];
-  const long long c = (long long)(blockIdx.x - d.block0) * blockDim.x + threadIdx.x;
-  if (c < d.count) {
-    const int cx = (int)(c % d.ext[0]);
-    const long long rr = c / d.ext[0];
-    const int cy = (int)(rr % d.ext[1]);
-    const int cz = (int)(rr / d.ext[1]);
+  const unsigned c = (blockIdx.x - (unsigned)d.block0) * blockDim.x + threadIdx.x;
+  if (c < (unsigned)d.count) {
+    const unsigned ex = (unsigned)d.ext[0], ey = (unsigned)d.ext[1];
+    const unsigned rr = c / ex;
+    const int cx = (int)(c - rr * ex);
+    const unsigned czu = rr / ey;
+    const int cy = (int)(rr - czu * ey);
+    const int cz = (int)czu;
     const long long so = (long long)(d.src[2] + cz) * g.sz + (long long)(d.src[1] + cy) * g.sy + (d.src[0] + cx);
     const long long dof = (long long)(d.dst[2] + cz) * g.sz + (long long)(d.dst[1] + cy) * g.sy + (d.dst[0] + cx);
     const int p = (int)d.buf_off;
@@ -136,19 +138,23 @@ __global__ void __launch_bounds__(256) seg_kernel(Fields<T> F, Geom g, SegList L
   int s = 0;
   while (s + 1 < L.n && (int)blockIdx.x >= L.s[s + 1].block0) ++s;
   const SegDesc& d = L.s[s];
-  const long long c = (long long)(blockIdx.x - d.block0) * blockDim.x + threadIdx.x;
-  if (c >= d.count) return;
-  const int cx = (int)(c % d.ext[0]);
-  const long long rr = c / d.ext[0];
-  const int cy = (int)(rr % d.ext[1]);
-  const int cz = (int)(rr / d.ext[1]);
-  const long long so = (long long)(d.src[2] + cz) * g.sz + (long long)(d.src[1] + cy) * g.sy + (d.src[0] + cx);
-  const long long dof = (long long)(d.dst[2] + cz) * g.sz + (long long)(d.dst[1] + cy) * g.sy + (d.dst[0] + cx);
+  // 32-bit index math (a segment holds < 2^31 cells): 64-bit div/mod per cell dominated this kernel
+  const unsigned c = (blockIdx.x - (unsigned)d.block0) * blockDim.x + threadIdx.x;
+  if (c >= (unsigned)d.count) return;
+  const unsigned ex = (unsigned)d.ext[0], ey = (unsigned)d.ext[1];
+  const unsigned rr = c / ex;
+  const int cx = (int)(c - rr * ex);
+  const unsigned cz = rr / ey;
+  const int cy = (int)(rr - cz * ey);
+  const long long so = (long long)(d.src[2] + (int)cz) * g.sz + (long long)(d.src[1] + cy) * g.sy + (d.src[0] + cx);
+  const long long dof = (long long)(d.dst[2] + (int)cz) * g.sz + (long long)(d.dst[1] + cy) * g.sy + (d.dst[0] + cx);
+  T v[NF];
+#pragma unroll
+  for (int q = 0; q < NF; ++q) v[q] = KIND == SEG_UNPACK ? buf[d.buf_off + (long long)q * d.count + c] : F.f[q][so];
 #pragma unroll
   for (int q = 0; q < NF; ++q) {
-    if (KIND == SEG_SELF) F.f[q][dof] = F.f[q][so];
-    if (KIND == SEG_PACK) buf[d.buf_off + q * d.count + c] = F.f[q][so];
-    if (KIND == SEG_UNPACK) F.f[q][dof] = buf[d.buf_off + q * d.count + c];
+    if (KIND == SEG_SELF || KIND == SEG_UNPACK) F.f[q][dof] = v[q];
+    if (KIND == SEG_PACK) buf[d.buf_off + (long long)q * d.count + c] = v[q];
   }
 }
 

@@ -72,14 +72,23 @@ void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scra
 // start coordinate to be 16-byte aligned, so boxes start at x rounded down to 16 bytes and are
 // widened accordingly: halo box COLS x ROWS x 1 from (floor16(x0 - 3), y0 - 3, z), f_{k-1} box
 // PCOLS x TY x 1 from (floor16(x0), y0, z).
-constexpr int kZTX = 32, kZTY = 8;
+// Tile shapes (x, y) per dtype; B2_ZM_TX64 selects the FP64 tile width at build time (32: one
+// 256-thread CTA per SM with a 5-slot ring; 16: two 128-thread CTAs per SM with 4-slot rings).
+#ifndef B2_ZM_TX64
+#define B2_ZM_TX64 32
+#endif
+template <typename T>
+constexpr int zm_tx() { return sizeof(T) == 8 ? B2_ZM_TX64 : 32; }
+template <typename T>
+constexpr int zm_ty() { return 8; }
 template <typename T>
 constexpr int zm_ch() { return 16 / (int)sizeof(T); }
 template <typename T>
-constexpr int zm_cols() { return (kZTX + 6 + zm_ch<T>() - 1 + zm_ch<T>() - 1) / zm_ch<T>() * zm_ch<T>(); }
+constexpr int zm_cols() { return (zm_tx<T>() + 6 + zm_ch<T>() - 1 + zm_ch<T>() - 1) / zm_ch<T>() * zm_ch<T>(); }
 template <typename T>
-constexpr int zm_pcols() { return kZTX + zm_ch<T>(); }
-constexpr int zm_rows() { return kZTY + 6; }
+constexpr int zm_pcols() { return zm_tx<T>() + zm_ch<T>(); }
+template <typename T>
+constexpr int zm_rows() { return zm_ty<T>() + 6; }
 struct TmapSet {
   CUtensorMap halo[NF];  // fields of the state read with the stencil
   CUtensorMap prev[NF];  // fields of the other state (f_{k-1}, read pointwise)
@@ -88,7 +97,8 @@ template <typename T>
 bool zmarch_supported(const Geom& g, const Region& r);
 template <typename T>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm = nullptr);
+                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm = nullptr,
+                   const FlagSet* wait = nullptr, unsigned long long wait_seq = 0);
 
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 constexpr int kReduceVals = 5;      // min, max, sum, sum of squares, sum of exp

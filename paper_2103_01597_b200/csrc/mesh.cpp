@@ -376,8 +376,10 @@ mhd_status encode_tmaps(mhd_mesh* m) {
   const cuuint64_t dims[3] = {(cuuint64_t)m->L.sy, (cuuint64_t)(m->g.ny + 2 * MHD_RADIUS),
                               (cuuint64_t)(m->g.nz + 2 * MHD_RADIUS)};
   const cuuint64_t strides[2] = {(cuuint64_t)(m->L.sy * es), (cuuint64_t)(m->L.sz * es)};
-  const cuuint32_t halo_box[3] = {(cuuint32_t)(f64 ? zm_cols<double>() : zm_cols<float>()), (cuuint32_t)zm_rows(), 1};
-  const cuuint32_t prev_box[3] = {(cuuint32_t)(f64 ? zm_pcols<double>() : zm_pcols<float>()), (cuuint32_t)kZTY, 1};
+  const cuuint32_t halo_box[3] = {(cuuint32_t)(f64 ? zm_cols<double>() : zm_cols<float>()),
+                                  (cuuint32_t)(f64 ? zm_rows<double>() : zm_rows<float>()), 1};
+  const cuuint32_t prev_box[3] = {(cuuint32_t)(f64 ? zm_pcols<double>() : zm_pcols<float>()),
+                                  (cuuint32_t)(f64 ? zm_ty<double>() : zm_ty<float>()), 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   for (int s = 0; s < 2; ++s)
     for (int q = 0; q < NF; ++q) {
@@ -426,6 +428,7 @@ double seg_bytes(const SegList& L, size_t es) {
 // The update of one region of the subdomain.
 template <typename T>
 void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out, const RemoteMap<T>* rm = nullptr) {
+  if (r.ext[0] <= 0 || r.ext[1] <= 0 || r.ext[2] <= 0) return;
   const Fields<T> in = m->fields<T>(m->cur), out = m->fields<T>(1 - m->cur);
   const Coef<T> C = make_coef<T>(m->info, k, dt);
   const bool zm = m->variant != 1 && m->tmaps_ok && zmarch_supported<T>(m->g, r);
@@ -480,15 +483,19 @@ mhd_status halo_end(mhd_mesh* m) {
   return MHD_OK;
 }
 
-// Inner region and outer slabs: only axes split across ranks need the
-// remote halo; along unsplit axes the whole extent is inner (its halo is a self copy).
-void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer) {
+// Inner region and outer slabs: only axes split across ranks need the remote halo;
+// along unsplit axes the whole extent is inner (its halo is a self copy).  `thick` is the slab
+// width per axis: the radius r = 3 for the NCCL schedule, wider for the peer-memory schedule so
+// that the slabs run on the tiled kernel (a superset of the cells within r of a split boundary).
+void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer, const int thick_in[3]) {
   const int n[3] = {m->g.nx, m->g.ny, m->g.nz};
   bool split[3];
+  int thick[3];
   for (int a = 0; a < 3; ++a) {
     split[a] = m->P[a] > 1;
-    inner.lo[a] = split[a] ? MHD_RADIUS : 0;
-    inner.ext[a] = split[a] ? n[a] - 2 * MHD_RADIUS : n[a];
+    thick[a] = std::max(MHD_RADIUS, std::min(thick_in[a], n[a] / 2));
+    inner.lo[a] = split[a] ? thick[a] : 0;
+    inner.ext[a] = split[a] ? n[a] - 2 * thick[a] : n[a];
   }
   outer.clear();
   // slabs: z first (full x, y), then y (full x, inner z), then x (inner y, z)
@@ -501,13 +508,14 @@ void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer)
         r.lo[b] = lo[b];
         r.ext[b] = hi[b] - lo[b];
       }
-      r.lo[a] = side == 0 ? 0 : n[a] - MHD_RADIUS;
-      r.ext[a] = MHD_RADIUS;
-      outer.push_back(r);
+      r.lo[a] = side == 0 ? 0 : n[a] - thick[a];
+      r.ext[a] = thick[a];
+      if (r.ext[0] > 0 && r.ext[1] > 0 && r.ext[2] > 0) outer.push_back(r);
     }
-    lo[a] = MHD_RADIUS;
-    hi[a] = n[a] - MHD_RADIUS;
+    lo[a] = thick[a];
+    hi[a] = n[a] - thick[a];
   }
+  if (inner.ext[0] <= 0 || inner.ext[1] <= 0 || inner.ext[2] <= 0) inner.ext[0] = inner.ext[1] = inner.ext[2] = 0;
 }
 
 // Peer-memory exchange.  Per substep: wait until every neighbour finished its
@@ -535,12 +543,15 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   if (!m->halo_valid) p2p_halo_copy<T>(m);
   Region inner;
   std::vector<Region> outer;
-  split_regions(m, inner, outer);
+  const int thick[3] = {zm_tx<T>(), zm_ty<T>(), 8};
+  split_regions(m, inner, outer, thick);
   {
     PhaseTimer t(m, m->stream, MHD_PHASE_EXCHANGE, 0.0);
     launch_p2p_wait(m->stream, m->wt, m->seq);
     m->launches++;
   }
+  // boundary slabs: update + store into the neighbours' halos (the fused send), then publish;
+  // the inner segment needs no remote halo and runs while the neighbours proceed
   const RemoteMap<T> rm = m->remote_map<T>(1 - m->cur);
   for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, rhs_out ? nullptr : &rm);
   launch_p2p_signal(m->stream, m->sig, ++m->seq);
@@ -558,7 +569,8 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   if (st != MHD_OK) return st;
   Region inner;
   std::vector<Region> outer;
-  split_regions(m, inner, outer);
+  const int thick[3] = {MHD_RADIUS, MHD_RADIUS, MHD_RADIUS};
+  split_regions(m, inner, outer, thick);
   update_region<T>(m, inner, k, dt, rhs_out);
   st = halo_end<T>(m);
   if (st != MHD_OK) return st;

@@ -57,13 +57,15 @@ template <typename T, int TX, int TY>
 struct ZCfg {
   static constexpr int ES = (int)sizeof(T);
   static constexpr int COLS = zm_cols<T>();
-  static constexpr int ROWS = TY + 6;
+  static constexpr int ROWS = zm_rows<T>();
+  static_assert(TX == zm_tx<T>() && TY == zm_ty<T>(), "tile must match the TMA boxes");
   static constexpr int FSZ = (ROWS * COLS * ES + 127) / 128 * 128 / ES;  // 128-B aligned TMA destinations
   static constexpr int SLOT = NF * FSZ;
-  // FP64: 5 slots (one plane of prefetch), 1 CTA/SM.  FP32: 4 slots and 2 CTAs/SM, the other CTA
-  // covering the refill latency.
-  static constexpr int NSLOT = sizeof(T) == 8 ? 5 : 4;
-  static constexpr int MINB = sizeof(T) == 8 ? 1 : 2;
+  // 256-thread FP64 CTAs: 5 slots (one plane of prefetch), 1 CTA/SM.  Otherwise 4 slots and
+  // 2 CTAs/SM, the other CTA covering the refill latency.
+  static constexpr bool BIG = sizeof(T) == 8 && TX * TY >= 256;
+  static constexpr int NSLOT = BIG ? 5 : 4;
+  static constexpr int MINB = BIG ? 1 : 2;
   static constexpr int NT = TX * TY;
   static constexpr int CH = zm_ch<T>();
   static constexpr int PCOLS = zm_pcols<T>();
@@ -272,7 +274,8 @@ struct ZStep {
 template <typename T, int TX, int TY, int MODE, bool REMOTE>
 __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
     zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C, int k,
-                  T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm) {
+                  T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm,
+                  const __grid_constant__ FlagSet wt, unsigned long long wseq) {
   using Z = ZCfg<T, TX, TY>;
   // Dynamic shared memory starts at the (1024-B aligned) base of the CTA window (no static
   // shared memory in this kernel).  The pointer must stay visibly __shared__ so that the stencil
@@ -335,8 +338,21 @@ __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
 #pragma unroll
       for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
 
-  if (tid == 0)
+  if (tid == 0) {
+    // peer-memory exchange: the halo planes are written by the neighbours' previous update; wait
+    // until every neighbour has published it (and is done reading the buffer we write into)
+    for (int i = 0; i < wt.n; ++i) {
+      const long long t0 = clock64();
+      for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(wt.ptr[i]) : "memory");
+        if (v >= wseq) break;
+        __nanosleep(256);
+        if (clock64() - t0 > 40000000000LL) __trap();
+      }
+    }
     for (int P = first; P < first + Z::NSLOT && P <= ze + 2; ++P) issue(P);
+  }
   wait_plane(first);
   wait_plane(first + 1);
   wait_plane(first + 2);
@@ -375,17 +391,20 @@ constexpr int kNZC = 64;
 
 template <typename T, int MODE, bool REMOTE>
 void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm) {
-  using Z = ZCfg<T, kZTX, kZTY>;
+                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm, const FlagSet& wt,
+                unsigned long long wseq) {
+  constexpr int TXc = zm_tx<T>(), TYc = zm_ty<T>();
+  using Z = ZCfg<T, TXc, TYc>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(zmarch_kernel<T, kZTX, kZTY, MODE, REMOTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(zmarch_kernel<T, TXc, TYc, MODE, REMOTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Z::SMEM);
     attr = true;
   }
   const int nzc = r.ext[2] < kNZC ? r.ext[2] : kNZC;
-  dim3 grd((r.ext[0] + kZTX - 1) / kZTX, (r.ext[1] + kZTY - 1) / kZTY, (r.ext[2] + nzc - 1) / nzc);
-  zmarch_kernel<T, kZTX, kZTY, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm);
+  dim3 grd((r.ext[0] + TXc - 1) / TXc, (r.ext[1] + TYc - 1) / TYc, (r.ext[2] + nzc - 1) / nzc);
+  zmarch_kernel<T, TXc, TYc, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm, wt,
+                                                                          wseq);
 }
 
 }  // namespace
@@ -398,21 +417,27 @@ bool zmarch_supported(const Geom& g, const Region& r) {
 
 template <typename T>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm) {
+                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm, const FlagSet* wt,
+                   unsigned long long wseq) {
   RemoteMap<T> none;
+  FlagSet nowait;
+  nowait.n = 0;
+  const FlagSet& w = wt ? *wt : nowait;
   if (rhs_out)
-    launch_cfg<T, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none);
+    launch_cfg<T, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none, w, wseq);
   else if (rm)
-    launch_cfg<T, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm);
+    launch_cfg<T, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm, w, wseq);
   else
-    launch_cfg<T, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none);
+    launch_cfg<T, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none, w, wseq);
 }
 
 template bool zmarch_supported<float>(const Geom&, const Region&);
 template bool zmarch_supported<double>(const Geom&, const Region&);
 template void launch_zmarch<float>(cudaStream_t, const TmapSet&, const Fields<float>&, const Geom&, const Region&,
-                                   const Coef<float>&, int, float*, int, const RemoteMap<float>*);
+                                   const Coef<float>&, int, float*, int, const RemoteMap<float>*, const FlagSet*,
+                                   unsigned long long);
 template void launch_zmarch<double>(cudaStream_t, const TmapSet&, const Fields<double>&, const Geom&, const Region&,
-                                    const Coef<double>&, int, double*, int, const RemoteMap<double>*);
+                                    const Coef<double>&, int, double*, int, const RemoteMap<double>*, const FlagSet*,
+                                    unsigned long long);
 
 }  // namespace b2

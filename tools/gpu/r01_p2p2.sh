@@ -1,0 +1,6 @@
+set -x
+timeout 1200 python -m pytest tests/test_multigpu.py -q -x > gpurun_out/pytest_p2p2_mgpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_p2p2_mgpu.log
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 2 --e2e-steps 0 --exchange p2p > gpurun_out/bench_p2p2_m2.log 2>&1
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29543 bench.py --gpus 2 --e2e-steps 0 --exchange p2p --scaling strong --grid 512 > gpurun_out/bench_p2p2_m2_strong.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "kernel_variants or steps_parity_fp64 or substep" > gpurun_out/pytest_p2p2_1gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_p2p2_1gpu.log
+echo done
