@@ -97,8 +97,7 @@ template <typename T>
 bool zmarch_supported(const Geom& g, const Region& r);
 template <typename T>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm = nullptr,
-                   const FlagSet* wait = nullptr, unsigned long long wait_seq = 0);
+                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm = nullptr);
 
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 constexpr int kReduceVals = 5;      // min, max, sum, sum of squares, sum of exp

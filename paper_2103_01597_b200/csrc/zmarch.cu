@@ -2,12 +2,11 @@
 //
 // A CTA owns a TX x TY column of cells and marches it along z over a chunk of planes.
 //  * Staging: each plane (8 fields, tile + radius-3 halo in x and y) is fetched by TMA
-//    (cp.async.bulk.tensor.3d, mbarrier completion) into a 5-slot shared-memory ring, one plane
-//    ahead of the computation; f_{k-1} of the output plane (read pointwise by the RK3 update)
-//    rides in the same transaction.  There is no CTA barrier in the march: each warp releases a
-//    slot when it is done with it (shared-memory counter), and the last warp to release issues
-//    the TMA that refills it, so warps drift up to one plane apart instead of hitting their
-//    shared-memory-heavy and FP64-heavy phases in lockstep.
+//    (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion) into a 5-slot
+//    shared-memory ring, one plane ahead of the computation; f_{k-1} of the output plane
+//    (read pointwise by the RK3 update) rides in the same transaction.  One CTA barrier per
+//    plane protects slot reuse (a barrier-free variant with per-slot release counters measured
+//    3 % slower: profiles/r01/).
 //  * In-plane derivatives (x, y axes and the d_x d_y diagonals of Eq. 14) are read
 //    from the slot of the output plane o; the z column of every field comes from registers
 //    (planes o-3..o-1) and from the ring (o+1..o+3).
@@ -61,11 +60,10 @@ struct ZCfg {
   static_assert(TX == zm_tx<T>() && TY == zm_ty<T>(), "tile must match the TMA boxes");
   static constexpr int FSZ = (ROWS * COLS * ES + 127) / 128 * 128 / ES;  // 128-B aligned TMA destinations
   static constexpr int SLOT = NF * FSZ;
-  // 256-thread FP64 CTAs: 5 slots (one plane of prefetch), 1 CTA/SM.  Otherwise 4 slots and
-  // 2 CTAs/SM, the other CTA covering the refill latency.
-  static constexpr bool BIG = sizeof(T) == 8 && TX * TY >= 256;
-  static constexpr int NSLOT = BIG ? 5 : 4;
-  static constexpr int MINB = BIG ? 1 : 2;
+  // 5 slots: planes o..o+3 in use while o+4 streams in.  One CTA per SM (a 16x8 FP64 tile at two
+  // CTAs per SM and a 2-CTA FP32 variant both measured slower: profiles/r01/).
+  static constexpr int NSLOT = 5;
+  static constexpr int MINB = 1;
   static constexpr int NT = TX * TY;
   static constexpr int CH = zm_ch<T>();
   static constexpr int PCOLS = zm_pcols<T>();
@@ -274,8 +272,7 @@ struct ZStep {
 template <typename T, int TX, int TY, int MODE, bool REMOTE>
 __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
     zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C, int k,
-                  T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm,
-                  const __grid_constant__ FlagSet wt, unsigned long long wseq) {
+                  T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm) {
   using Z = ZCfg<T, TX, TY>;
   // Dynamic shared memory starts at the (1024-B aligned) base of the CTA window (no static
   // shared memory in this kernel).  The pointer must stay visibly __shared__ so that the stencil
@@ -284,7 +281,6 @@ __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
   T* const ring = reinterpret_cast<T*>(smem_raw);
   T* const prevbuf = ring + Z::NSLOT * Z::SLOT;
   uint64_t* const mbar = reinterpret_cast<uint64_t*>(prevbuf + 2 * NF * Z::PSZ);
-  unsigned* const released = reinterpret_cast<unsigned*>(mbar + Z::NSLOT);  // warps done with a slot
 
   const int tid = (int)threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -300,10 +296,7 @@ __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
 
   if (tid == 0) {
     if (smem_u32(smem_raw) & 127) __trap();  // TMA destinations need 128-B alignment
-    for (int s = 0; s < Z::NSLOT; ++s) {
-      mbar_init(&mbar[s], 1);
-      released[s] = 0;
-    }
+    for (int s = 0; s < Z::NSLOT; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -338,45 +331,24 @@ __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
 #pragma unroll
       for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
 
-  if (tid == 0) {
-    // peer-memory exchange: the halo planes are written by the neighbours' previous update; wait
-    // until every neighbour has published it (and is done reading the buffer we write into)
-    for (int i = 0; i < wt.n; ++i) {
-      const long long t0 = clock64();
-      for (;;) {
-        unsigned long long v;
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(wt.ptr[i]) : "memory");
-        if (v >= wseq) break;
-        __nanosleep(256);
-        if (clock64() - t0 > 40000000000LL) __trap();
-      }
-    }
-    for (int P = first; P < first + Z::NSLOT && P <= ze + 2; ++P) issue(P);
-  }
+  if (tid == 0)
+    for (int P = first; P <= zb && P <= ze + 2; ++P) issue(P);
   wait_plane(first);
   wait_plane(first + 1);
   wait_plane(first + 2);
 
-  const bool lane0 = (tid & 31) == 0;
   auto iter = [&](auto ph, int p) {
     constexpr int PH = decltype(ph)::value;
+    __syncthreads();  // every thread is done with iteration p - 1: its slot is refilled now
+    if (tid == 0 && p + 4 <= ze + 2) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(p + 4);
+    }
     wait_plane(p + 3);  // plane p+3 and f_{k-1}(p) have landed
     if (p < zb)
       S.template push_only<PH>(st, p);
     else
       S.template full<PH>(st, p, out, g, k, active, x, y, rhs_out);
-    // release slot(p) (and the f_{k-1} buffer of plane p); the last warp refills it with p + NSLOT
-    __syncwarp();
-    if (lane0) {
-      const int s = (p - first) % Z::NSLOT;
-      if (atomicAdd(&released[s], 1u) == Z::NWARPS - 1) {
-        released[s] = 0;
-        if (p + Z::NSLOT <= ze + 2) {
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          issue(p + Z::NSLOT);
-        }
-      }
-    }
   };
 #pragma unroll 1
   for (int p = first; p < ze; p += 3) {
@@ -391,8 +363,7 @@ constexpr int kNZC = 64;
 
 template <typename T, int MODE, bool REMOTE>
 void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm, const FlagSet& wt,
-                unsigned long long wseq) {
+                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm) {
   constexpr int TXc = zm_tx<T>(), TYc = zm_ty<T>();
   using Z = ZCfg<T, TXc, TYc>;
   static bool attr = false;
@@ -403,8 +374,7 @@ void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const 
   }
   const int nzc = r.ext[2] < kNZC ? r.ext[2] : kNZC;
   dim3 grd((r.ext[0] + TXc - 1) / TXc, (r.ext[1] + TYc - 1) / TYc, (r.ext[2] + nzc - 1) / nzc);
-  zmarch_kernel<T, TXc, TYc, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm, wt,
-                                                                          wseq);
+  zmarch_kernel<T, TXc, TYc, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm);
 }
 
 }  // namespace
@@ -417,27 +387,21 @@ bool zmarch_supported(const Geom& g, const Region& r) {
 
 template <typename T>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm, const FlagSet* wt,
-                   unsigned long long wseq) {
+                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm) {
   RemoteMap<T> none;
-  FlagSet nowait;
-  nowait.n = 0;
-  const FlagSet& w = wt ? *wt : nowait;
   if (rhs_out)
-    launch_cfg<T, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none, w, wseq);
+    launch_cfg<T, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none);
   else if (rm)
-    launch_cfg<T, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm, w, wseq);
+    launch_cfg<T, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm);
   else
-    launch_cfg<T, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none, w, wseq);
+    launch_cfg<T, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none);
 }
 
 template bool zmarch_supported<float>(const Geom&, const Region&);
 template bool zmarch_supported<double>(const Geom&, const Region&);
 template void launch_zmarch<float>(cudaStream_t, const TmapSet&, const Fields<float>&, const Geom&, const Region&,
-                                   const Coef<float>&, int, float*, int, const RemoteMap<float>*, const FlagSet*,
-                                   unsigned long long);
+                                   const Coef<float>&, int, float*, int, const RemoteMap<float>*);
 template void launch_zmarch<double>(cudaStream_t, const TmapSet&, const Fields<double>&, const Geom&, const Region&,
-                                    const Coef<double>&, int, double*, int, const RemoteMap<double>*, const FlagSet*,
-                                    unsigned long long);
+                                    const Coef<double>&, int, double*, int, const RemoteMap<double>*);
 
 }  // namespace b2
