@@ -100,50 +100,50 @@ def get_threads() -> int:
 
 
 # --- grid helpers ------------------------------------------------------------------------------
-def with_halo(interior: np.ndarray) -> np.ndarray:
-    """Embed an interior (nz, ny, nx) array into a zero (nz+6, ny+6, nx+6) grid."""
+def with_halo(interior: np.ndarray, r: int = R) -> np.ndarray:
+    """Embed an interior (nz, ny, nx) array into a zero (nz+2r, ny+2r, nx+2r) grid."""
     nz, ny, nx = interior.shape
-    g = np.zeros((nz + 2 * R, ny + 2 * R, nx + 2 * R), dtype=interior.dtype)
-    g[R:R + nz, R:R + ny, R:R + nx] = interior
+    g = np.zeros((nz + 2 * r, ny + 2 * r, nx + 2 * r), dtype=interior.dtype)
+    g[r:r + nz, r:r + ny, r:r + nx] = interior
     return g
 
 
-def periodic_fill(grid: np.ndarray, kind: str = "d") -> np.ndarray:
-    """P:705 halo map on one halo-inclusive field (in place, returned)."""
+def periodic_fill(grid: np.ndarray, kind: str = "d", r: int = R) -> np.ndarray:
+    """P:705 halo map on one halo-inclusive field of halo width r (in place, returned)."""
     g = np.ascontiguousarray(grid, dtype=_dtype(kind))
-    nz, ny, nx = (s - 2 * R for s in g.shape)
-    _lib(kind).oracle_periodic_fill(_ptr(g), nx, ny, nz)
+    nz, ny, nx = (s - 2 * r for s in g.shape)
+    _lib(kind).oracle_periodic_fill(_ptr(g), nx, ny, nz, r)
     return g
 
 
-def apply_op(grid: np.ndarray, ds, op: str, a1: int, a2: int = 0, kind: str = "d") -> np.ndarray:
-    """6th-order operator on a halo-filled field at every interior cell.
+def apply_op(grid: np.ndarray, ds, op: str, a1: int, a2: int = 0, kind: str = "d", r: int = R) -> np.ndarray:
+    """Order-2r central-difference operator on a halo-filled field at every interior cell.
 
     op: 'd1' (first derivative along axis a1), 'd2' (second along a1), 'dx' (cross a1, a2).
     Axes: 0 = x (fastest), 1 = y, 2 = z.
     """
     g = np.ascontiguousarray(grid, dtype=_dtype(kind))
-    nz, ny, nx = (s - 2 * R for s in g.shape)
+    nz, ny, nx = (s - 2 * r for s in g.shape)
     out = np.empty((nz, ny, nx), dtype=_dtype(kind))
     code = {"d1": 1, "d2": 2, "dx": 3}[op]
-    _lib(kind).oracle_apply_op(_ptr(g), nx, ny, nz, _ds(ds), code, a1, a2, _ptr(out))
+    _lib(kind).oracle_apply_op(_ptr(g), nx, ny, nz, r, _ds(ds), code, a1, a2, _ptr(out))
     return out
 
 
-def rhs(state: np.ndarray, ds, params, kind: str = "d") -> np.ndarray:
-    """RHS (B.1-B.4) of an interior state of shape (8, nz, ny, nx), periodic."""
+def rhs(state: np.ndarray, ds, params, kind: str = "d", r: int = R) -> np.ndarray:
+    """RHS (B.1-B.4) of an interior state of shape (8, nz, ny, nx), periodic, order 2r."""
     st = [np.ascontiguousarray(state[q], dtype=_dtype(kind)) for q in range(NF)]
     nz, ny, nx = st[0].shape
     out = [np.empty((nz, ny, nx), dtype=_dtype(kind)) for _ in range(NF)]
     p = _params(params)
-    rc = _lib(kind).oracle_rhs_of_state(_ptrs(st), nx, ny, nz, _ds(ds), ctypes.byref(p), _ptrs(out))
+    rc = _lib(kind).oracle_rhs_of_state(_ptrs(st), nx, ny, nz, r, _ds(ds), ctypes.byref(p), _ptrs(out))
     if rc != 0:
         raise MemoryError("oracle_rhs_of_state")
     return np.stack(out)
 
 
 def integrate(state: np.ndarray, ds, params, dt: float, nsteps: int, substeps: int | None = None,
-              kind: str = "d", return_rhs: bool = False):
+              kind: str = "d", return_rhs: bool = False, r: int = R):
     """Run nsteps RK3 steps (or exactly `substeps` substeps) from an interior state (8, nz, ny, nx).
 
     Returns the new state (and the RHS of the last substep if return_rhs).
@@ -152,7 +152,7 @@ def integrate(state: np.ndarray, ds, params, dt: float, nsteps: int, substeps: i
     nz, ny, nx = st[0].shape
     rh = [np.empty((nz, ny, nx), dtype=_dtype(kind)) for _ in range(NF)]
     p = _params(params)
-    rc = _lib(kind).oracle_integrate(_ptrs(st), nx, ny, nz, _ds(ds), ctypes.byref(p), ctypes.c_double(dt),
+    rc = _lib(kind).oracle_integrate(_ptrs(st), nx, ny, nz, r, _ds(ds), ctypes.byref(p), ctypes.c_double(dt),
                                      int(nsteps), -1 if substeps is None else int(substeps), _ptrs(rh))
     if rc != 0:
         raise MemoryError("oracle_integrate")

@@ -20,13 +20,15 @@
  *   Grid, halo, radius r ............ P:108-112 (Eq. 1), P:194-211 (Eqs. 2-3)
  *   Periodic halo map s' = ((s-r) mod n') + r ... P:705 (§3.3)
  *   Stencil point set (axes + in-plane diagonals) P:832-836 (Eq. 14)
- *   6th-order central differences ... P:829-830 (§4); weights R#1, R#2
+ *   central differences, order 2r ... P:829-830 (§4); weights R#1, R#2
  *   RK3, Williamson 2N storage ...... P:830 (§4); coefficients R#3
  *   MHD equations B.1-B.4 ........... P:1092-1111 (App. B); EOS R#5, R#6
  *
- * Layout: each field is an array of (nz+2R)(ny+2R)(nx+2R) values, x fastest,
- * with a halo of R = 3 cells on every side; "interior" arrays are nz*ny*nx,
+ * Layout: each field is an array of (nz+2r)(ny+2r)(nx+2r) values, x fastest,
+ * with a halo of r cells on every side; "interior" arrays are nz*ny*nx,
  * x fastest.  Field order: lnrho, ux, uy, uz, s, Ax, Ay, Az (R#14).
+ * The radius r = 1, 2, 3, 4 selects 2nd-, 4th-, 6th- or 8th-order central
+ * differences ("2nd-, 4th-, 6th-, and 8th-order"; k = 2r).
  */
 #include <math.h>
 #include <stdlib.h>
@@ -41,7 +43,7 @@ typedef double real;
 #define EXP exp
 #endif
 
-#define R 3          /* stencil radius r = 3 for 6th order, "k = 2r" */
+#define RMAX 4       /* largest stencil radius: 8th order (k = 2r) */
 #define NF 8         /* eight scalar fields, Table B.1 */
 
 enum { LNRHO = 0, UX, UY, UZ, SS, AX, AY, AZ };
@@ -51,42 +53,54 @@ typedef struct {
 } oracle_params;
 
 /* ---- grid indexing (M = N + 2r per axis) ---------------------- */
-typedef struct { int nx, ny, nz; } dims3;
+typedef struct { int nx, ny, nz, r; } dims3;
 
 static size_t gidx(dims3 d, int x, int y, int z) {
-  /* x, y, z are halo-inclusive coordinates in [0, n+2R) */
-  return ((size_t)z * (size_t)(d.ny + 2 * R) + (size_t)y) * (size_t)(d.nx + 2 * R) + (size_t)x;
+  /* x, y, z are halo-inclusive coordinates in [0, n+2r) */
+  return ((size_t)z * (size_t)(d.ny + 2 * d.r) + (size_t)y) * (size_t)(d.nx + 2 * d.r) + (size_t)x;
 }
 
-size_t oracle_grid_cells(int nx, int ny, int nz) {
-  return (size_t)(nx + 2 * R) * (size_t)(ny + 2 * R) * (size_t)(nz + 2 * R);
+size_t oracle_grid_cells(int nx, int ny, int nz, int r) {
+  return (size_t)(nx + 2 * r) * (size_t)(ny + 2 * r) * (size_t)(nz + 2 * r);
 }
 
 /* ---- periodic halo (s'_i = ((s_i - r) mod n'_i) + r; P:418 periodic) -
  * Every halo cell, sides, edges and corners alike, takes the value of the
  * interior cell at the wrapped index along each axis. */
-static int wrap(int s, int n) { int m = (s - R) % n; if (m < 0) m += n; return m + R; }
+static int wrap(int s, int n, int r) { int m = (s - r) % n; if (m < 0) m += n; return m + r; }
 
-void oracle_periodic_fill(real* f, int nx, int ny, int nz) {
-  dims3 d = {nx, ny, nz};
-  for (int z = 0; z < nz + 2 * R; ++z)
-    for (int y = 0; y < ny + 2 * R; ++y)
-      for (int x = 0; x < nx + 2 * R; ++x) {
-        int inside = x >= R && x < nx + R && y >= R && y < ny + R && z >= R && z < nz + R;
-        if (!inside) f[gidx(d, x, y, z)] = f[gidx(d, wrap(x, nx), wrap(y, ny), wrap(z, nz))];
+void oracle_periodic_fill(real* f, int nx, int ny, int nz, int r) {
+  dims3 d = {nx, ny, nz, r};
+  for (int z = 0; z < nz + 2 * r; ++z)
+    for (int y = 0; y < ny + 2 * r; ++y)
+      for (int x = 0; x < nx + 2 * r; ++x) {
+        int inside = x >= r && x < nx + r && y >= r && y < ny + r && z >= r && z < nz + r;
+        if (!inside) f[gidx(d, x, y, z)] = f[gidx(d, wrap(x, nx, r), wrap(y, ny, r), wrap(z, nz, r))];
       }
 }
 
-/* ---- 6th-order central differences (weights R#1, R#2) ----------
- * First derivative:  D1 f = sum_i c_i (f(+i) - f(-i)) / ds,  c = (3/4, -3/20, 1/60)
- * Second derivative: D2 f = sum_i d_i ((f(+i) - f0) + (f(-i) - f0)) / ds^2,
- *                    d = (3/2, -3/20, 1/90)   (difference form of c0 = -49/18)
+/* ---- central differences of order 2r (weights R#1, R#2) --------
+ * First derivative:  D1 f = sum_i c_i (f(+i) - f(-i)) / ds
+ * Second derivative: D2 f = sum_i d_i ((f(+i) - f0) + (f(-i) - f0)) / ds^2   (difference form)
  * Cross derivative:  DX f = sum_i e_i (f(+i,+i) + f(-i,-i) - f(+i,-i) - f(-i,+i)) / (da db),
- *                    e = (270, -27, 2)/720 — uses only the in-plane diagonal
- *                    points z(x +- y) of Eq. 14. */
-static const real C1[4] = {0, (real)3 / 4, -(real)3 / 20, (real)1 / 60};
-static const real C2[4] = {0, (real)3 / 2, -(real)3 / 20, (real)1 / 90};
-static const real CX[4] = {0, (real)270 / 720, -(real)27 / 720, (real)2 / 720};
+ *                    e_i = d_i / 4, using only the in-plane diagonal points z(x +- y) of
+ *                    Eq. 14.  Textbook central-difference weights, i = 1..r:
+ *   r = 1: c = (1/2)                         d = (1)
+ *   r = 2: c = (2/3, -1/12)                  d = (4/3, -1/12)
+ *   r = 3: c = (3/4, -3/20, 1/60)            d = (3/2, -3/20, 1/90)
+ *   r = 4: c = (4/5, -1/5, 4/105, -1/280)    d = (8/5, -1/5, 8/315, -1/560) */
+static const real C1T[RMAX + 1][RMAX + 1] = {
+    {0},
+    {0, (real)1 / 2},
+    {0, (real)2 / 3, -(real)1 / 12},
+    {0, (real)3 / 4, -(real)3 / 20, (real)1 / 60},
+    {0, (real)4 / 5, -(real)1 / 5, (real)4 / 105, -(real)1 / 280}};
+static const real C2T[RMAX + 1][RMAX + 1] = {
+    {0},
+    {0, 1},
+    {0, (real)4 / 3, -(real)1 / 12},
+    {0, (real)3 / 2, -(real)3 / 20, (real)1 / 90},
+    {0, (real)8 / 5, -(real)1 / 5, (real)8 / 315, -(real)1 / 560}};
 
 typedef struct { const real* f; dims3 d; } fieldv;
 
@@ -98,25 +112,25 @@ static void axis_step(int axis, int i, int* dx, int* dy, int* dz) {
 
 static real d1(fieldv g, int x, int y, int z, int axis, const double ds[3]) {
   real acc = 0;
-  for (int i = 1; i <= R; ++i) {
+  for (int i = 1; i <= g.d.r; ++i) {
     int a, b, c; axis_step(axis, i, &a, &b, &c);
-    acc += C1[i] * (at(g, x + a, y + b, z + c) - at(g, x - a, y - b, z - c));
+    acc += C1T[g.d.r][i] * (at(g, x + a, y + b, z + c) - at(g, x - a, y - b, z - c));
   }
   return acc / (real)ds[axis];
 }
 
 static real d2(fieldv g, int x, int y, int z, int axis, const double ds[3]) {
   real f0 = at(g, x, y, z), acc = 0;
-  for (int i = 1; i <= R; ++i) {
+  for (int i = 1; i <= g.d.r; ++i) {
     int a, b, c; axis_step(axis, i, &a, &b, &c);
-    acc += C2[i] * ((at(g, x + a, y + b, z + c) - f0) + (at(g, x - a, y - b, z - c) - f0));
+    acc += C2T[g.d.r][i] * ((at(g, x + a, y + b, z + c) - f0) + (at(g, x - a, y - b, z - c) - f0));
   }
   return acc / ((real)ds[axis] * (real)ds[axis]);
 }
 
 static real dx2(fieldv g, int x, int y, int z, int ax1, int ax2, const double ds[3]) {
   real acc = 0;
-  for (int i = 1; i <= R; ++i) {
+  for (int i = 1; i <= g.d.r; ++i) {
     int a1, b1, c1, a2, b2, c2;
     axis_step(ax1, i, &a1, &b1, &c1);
     axis_step(ax2, i, &a2, &b2, &c2);
@@ -124,7 +138,7 @@ static real dx2(fieldv g, int x, int y, int z, int ax1, int ax2, const double ds
     real mm = at(g, x - a1 - a2, y - b1 - b2, z - c1 - c2);
     real pm = at(g, x + a1 - a2, y + b1 - b2, z + c1 - c2);
     real mp = at(g, x - a1 + a2, y - b1 + b2, z - c1 + c2);
-    acc += CX[i] * (pp + mm - pm - mp);
+    acc += C2T[g.d.r][i] / 4 * (pp + mm - pm - mp);
   }
   return acc / ((real)ds[ax1] * (real)ds[ax2]);
 }
@@ -136,9 +150,10 @@ static real dd(fieldv g, int x, int y, int z, int a, int b, const double ds[3]) 
 
 /* Operator on a halo-filled field, evaluated at every interior cell.
  * op: 1 = D1 along a1; 2 = D2 along a1; 3 = cross derivative (a1, a2). */
-void oracle_apply_op(const real* f, int nx, int ny, int nz, const double ds[3],
+void oracle_apply_op(const real* f, int nx, int ny, int nz, int r, const double ds[3],
                      int op, int a1, int a2, real* out) {
-  dims3 d = {nx, ny, nz};
+  dims3 d = {nx, ny, nz, r};
+  const int R = r;
   fieldv g = {f, d};
   for (int z = 0; z < nz; ++z)
     for (int y = 0; y < ny; ++y)
@@ -251,9 +266,10 @@ static void rhs_cell(fieldv g[NF], int x, int y, int z, const double ds[3],
 }
 
 /* RHS at every interior cell.  f: 8 halo-filled fields; rhs: 8 interior arrays. */
-void oracle_rhs(real* const f[NF], int nx, int ny, int nz, const double ds[3],
+void oracle_rhs(real* const f[NF], int nx, int ny, int nz, int r, const double ds[3],
                 const oracle_params* p, real* const rhs[NF]) {
-  dims3 d = {nx, ny, nz};
+  dims3 d = {nx, ny, nz, r};
+  const int R = r;
   fieldv g[NF];
   for (int k = 0; k < NF; ++k) { g[k].f = f[k]; g[k].d = d; }
 #pragma omp parallel for schedule(static)
@@ -296,11 +312,12 @@ void oracle_rk3_linear(real* y, size_t n, double lambda, double dt, int nsteps) 
  * stop_substep: if >= 0, stop after that many substeps in total (for substep-level
  * parity), else run 3*nsteps substeps.
  * rhs_out: optional 8 interior arrays receiving the RHS of the last substep run. */
-int oracle_integrate(real* const state[NF], int nx, int ny, int nz, const double ds[3],
+int oracle_integrate(real* const state[NF], int nx, int ny, int nz, int r, const double ds[3],
                      const oracle_params* p, double dt, int nsteps, int stop_substep,
                      real* const rhs_out[NF]) {
-  size_t ncell = (size_t)nx * ny * nz, ngrid = oracle_grid_cells(nx, ny, nz);
-  dims3 d = {nx, ny, nz};
+  size_t ncell = (size_t)nx * ny * nz, ngrid = oracle_grid_cells(nx, ny, nz, r);
+  dims3 d = {nx, ny, nz, r};
+  const int R = r;
   real* f[NF]; real* w[NF]; real* rhs[NF];
   for (int k = 0; k < NF; ++k) {
     f[k] = (real*)calloc(ngrid, sizeof(real));
@@ -315,9 +332,9 @@ int oracle_integrate(real* const state[NF], int nx, int ny, int nz, const double
       for (int z = 0; z < nz; ++z)
         for (int y = 0; y < ny; ++y)
           memcpy(&f[q][gidx(d, R, y + R, z + R)], &state[q][((size_t)z * ny + y) * nx], nx * sizeof(real));
-      oracle_periodic_fill(f[q], nx, ny, nz);        /* halo exchange */
+      oracle_periodic_fill(f[q], nx, ny, nz, r);     /* halo exchange */
     }
-    oracle_rhs(f, nx, ny, nz, ds, p, rhs);             /* all cells before any update */
+    oracle_rhs(f, nx, ny, nz, r, ds, p, rhs);          /* all cells before any update */
     for (int q = 0; q < NF; ++q) oracle_rk3_update(state[q], w[q], rhs[q], ncell, k, dt);
   }
   if (rhs_out)
@@ -327,10 +344,11 @@ int oracle_integrate(real* const state[NF], int nx, int ny, int nz, const double
 }
 
 /* RHS of an interior state (periodic), without any update: the `debug_rhs` check. */
-int oracle_rhs_of_state(real* const state[NF], int nx, int ny, int nz, const double ds[3],
+int oracle_rhs_of_state(real* const state[NF], int nx, int ny, int nz, int r, const double ds[3],
                         const oracle_params* p, real* const rhs_out[NF]) {
-  size_t ngrid = oracle_grid_cells(nx, ny, nz);
-  dims3 d = {nx, ny, nz};
+  size_t ngrid = oracle_grid_cells(nx, ny, nz, r);
+  dims3 d = {nx, ny, nz, r};
+  const int R = r;
   real* f[NF];
   for (int q = 0; q < NF; ++q) {
     f[q] = (real*)calloc(ngrid, sizeof(real));
@@ -338,9 +356,9 @@ int oracle_rhs_of_state(real* const state[NF], int nx, int ny, int nz, const dou
     for (int z = 0; z < nz; ++z)
       for (int y = 0; y < ny; ++y)
         memcpy(&f[q][gidx(d, R, y + R, z + R)], &state[q][((size_t)z * ny + y) * nx], nx * sizeof(real));
-    oracle_periodic_fill(f[q], nx, ny, nz);
+    oracle_periodic_fill(f[q], nx, ny, nz, r);
   }
-  oracle_rhs(f, nx, ny, nz, ds, p, rhs_out);
+  oracle_rhs(f, nx, ny, nz, r, ds, p, rhs_out);
   for (int q = 0; q < NF; ++q) free(f[q]);
   return 0;
 }
