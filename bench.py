@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--corners", action="store_true")
+    ap.add_argument("--order", type=int, choices=(2, 4, 6, 8), default=6,
+                    help="stencil order 2r (P:829-830); the paper's benchmarks use 6")
     ap.add_argument("--exchange", choices=("p2p", "nccl"), default="nccl",
                     help="N > 1: fused peer-memory boundary stores (p2p) or NCCL send/recv of packed segments")
     return ap.parse_args()
@@ -209,7 +211,7 @@ def main():
     es = 8 if dtype == b2.MHD_F64 else 4
     ds = synth.spacing(n_glob)
     mesh = b2.Mesh(n_glob, ds, synth.P0, dtype, rank=rank, nranks=world, exchange_corners=args.corners,
-                   kernel=args.kernel, exchange=args.exchange)
+                   kernel=args.kernel, exchange=args.exchange, radius=args.order // 2)
     nz, ny, nx = mesh.shape
     lo = tuple(c * n for c, n in zip(reversed(mesh.coord), (nz, ny, nx)))
     npdt = np.float64 if dtype == b2.MHD_F64 else np.float32
@@ -319,7 +321,7 @@ def main():
                        "substeps_per_step": 3, "dt": dt, "params": "P0",
                        "l2": "inputs larger than L2 (no flush)", "kernel": args.kernel,
                        "exchange_corners": bool(args.corners),
-                       "exchange": mesh.exchange},
+                       "exchange": mesh.exchange, "order": args.order},
             "ms_per_substep": substep_ms,
             "gpu_launches": launches,
             "clocks": clk.summary(),

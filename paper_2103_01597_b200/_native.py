@@ -106,13 +106,13 @@ def check(status: int, where: str) -> None:
 
 
 def make_info(n_xyz, ds_xyz, params: dict, dtype: int = MHD_F64, rank: int = 0, nranks: int = 1,
-              exchange_corners: bool = False) -> mhd_mesh_info:
+              exchange_corners: bool = False, radius: int = MHD_RADIUS) -> mhd_mesh_info:
     info = mhd_mesh_info()
     info.abi_version = MHD_ABI_VERSION
     for a in range(3):
         info.n[a] = int(n_xyz[a])
         info.ds[a] = float(ds_xyz[a])
-    info.radius = MHD_RADIUS
+    info.radius = int(radius)  # stencil order 2r: 2, 4, 6 or 8
     info.dtype = int(dtype)
     info.rank = int(rank)
     info.nranks = int(nranks)

@@ -22,7 +22,7 @@ struct GAcc {
 
 // MODE 0: RK3 update into `out` (which holds f_{k-1} for k > 0); MODE 1: RHS to rhs_out.
 // REMOTE: also deliver the new boundary values into the neighbours' halos (remote.cuh).
-template <typename T, int MODE, bool REMOTE>
+template <typename T, int RAD, int MODE, bool REMOTE>
 __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out, Geom g, Region r, Coef<T> C,
                                                      int k, T* __restrict__ rhs_out, RemoteMap<T> rm) {
   const int x = r.lo[0] + blockIdx.x * blockDim.x + threadIdx.x;
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out
   const long long base = (long long)z * g.sz + (long long)y * g.sy + x;
   GAcc<T> V{in, base, g.sy, g.sz};
   Derivs<T> D;
-  gather<T>(V, C, D);
+  gather<T, RAD>(V, C, D);
   T rhs[NF];
   rhs_cell<T>(D, C, rhs);
   if (MODE == 0) {
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out
       out.f[q][base] = fn[q];
     }
     if (REMOTE) {
-      remote_store<T>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, z, fn);
+      remote_store<T, RAD>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, z, fn);
       __threadfence_system();
     }
   } else {
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out
   }
 }
 
-template <typename T>
+template <typename T, int RAD>
 void launch_direct(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, const Geom& g, const Region& r,
                    const Coef<T>& C, int k, T* rhs_out, const RemoteMap<T>* rm) {
   if (r.ext[0] <= 0 || r.ext[1] <= 0 || r.ext[2] <= 0) return;
@@ -64,11 +64,11 @@ void launch_direct(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, c
   dim3 grd((r.ext[0] + blk.x - 1) / blk.x, (r.ext[1] + blk.y - 1) / blk.y, (r.ext[2] + blk.z - 1) / blk.z);
   RemoteMap<T> none;
   if (rhs_out)
-    direct_kernel<T, 1, false><<<grd, blk, 0, st>>>(in, out, g, r, C, k, rhs_out, none);
+    direct_kernel<T, RAD, 1, false><<<grd, blk, 0, st>>>(in, out, g, r, C, k, rhs_out, none);
   else if (rm)
-    direct_kernel<T, 0, true><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr, *rm);
+    direct_kernel<T, RAD, 0, true><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr, *rm);
   else
-    direct_kernel<T, 0, false><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr, none);
+    direct_kernel<T, RAD, 0, false><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr, none);
 }
 
 // ---- peer-memory exchange helpers -------------------------------------------------------------------
@@ -256,9 +256,19 @@ void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scra
 }
 
 // ---- explicit instantiations ----------------------------------------------------------------------
+#define B2_DIRECT(T, RAD)                                                                               \
+  template void launch_direct<T, RAD>(cudaStream_t, const Fields<T>&, const Fields<T>&, const Geom&,      \
+                                      const Region&, const Coef<T>&, int, T*, const RemoteMap<T>*);
+B2_DIRECT(float, 1)
+B2_DIRECT(float, 2)
+B2_DIRECT(float, 3)
+B2_DIRECT(float, 4)
+B2_DIRECT(double, 1)
+B2_DIRECT(double, 2)
+B2_DIRECT(double, 3)
+B2_DIRECT(double, 4)
+#undef B2_DIRECT
 #define B2_INST(T)                                                                                       \
-  template void launch_direct<T>(cudaStream_t, const Fields<T>&, const Fields<T>&, const Geom&,           \
-                                 const Region&, const Coef<T>&, int, T*, const RemoteMap<T>*);            \
   template void launch_remote_copy<T>(cudaStream_t, const Fields<T>&, const Geom&, const SegList&,        \
                                       const RemoteMap<T>&);                                              \
   template void launch_segments<T>(cudaStream_t, const Fields<T>&, const Geom&, const SegList&, int, T*); \

@@ -46,7 +46,7 @@ struct Region {
 };
 
 // ---- launchers (kernels.cu) ----
-template <typename T>
+template <typename T, int RAD>
 void launch_direct(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, const Geom& g,
                    const Region& r, const Coef<T>& C, int k, T* rhs_out, const RemoteMap<T>* rm = nullptr);
 // peer-memory exchange: copy the remote segments of a state into the peers' halos; flags
@@ -67,35 +67,30 @@ void launch_copy_out(cudaStream_t st, const TS* origin, TD* dst, const Geom& g);
 template <typename T>
 void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scratch, int nblocks);
 
-// ---- z-marching TMA kernel (zmarch.cu) ----
-// Tile of a CTA and the TMA boxes it stages per plane and field.  TMA requires the innermost
-// start coordinate to be 16-byte aligned, so boxes start at x rounded down to 16 bytes and are
-// widened accordingly: halo box COLS x ROWS x 1 from (floor16(x0 - 3), y0 - 3, z), f_{k-1} box
-// PCOLS x TY x 1 from (floor16(x0), y0, z).
-// Tile shapes (x, y) per dtype; B2_ZM_TX64 selects the FP64 tile width at build time (32: one
-// 256-thread CTA per SM with a 5-slot ring; 16: two 128-thread CTAs per SM with 4-slot rings).
-#ifndef B2_ZM_TX64
-#define B2_ZM_TX64 32
-#endif
+// ---- z-marching TMA kernel (zmarch.cuh, one instantiation per dtype and radius) ----
+// TMA boxes per plane and field.  TMA requires the innermost start coordinate to be 16-byte
+// aligned, so boxes start at x rounded down to 16 bytes and are widened accordingly: halo box
+// COLS x ROWS x 1 from (floor16(x0 - r), y0 - r, z), f_{k-1} box PCOLS x TY x 1 from (floor16(x0), y0, z).
+// Tile of a CTA: 32 x 8 cells (a 16 x 8 FP64 tile at two CTAs per SM measured slower).
 template <typename T>
-constexpr int zm_tx() { return sizeof(T) == 8 ? B2_ZM_TX64 : 32; }
+constexpr int zm_tx() { return 32; }
 template <typename T>
 constexpr int zm_ty() { return 8; }
 template <typename T>
 constexpr int zm_ch() { return 16 / (int)sizeof(T); }
-template <typename T>
-constexpr int zm_cols() { return (zm_tx<T>() + 6 + zm_ch<T>() - 1 + zm_ch<T>() - 1) / zm_ch<T>() * zm_ch<T>(); }
+template <typename T, int RAD>
+constexpr int zm_cols() { return (zm_tx<T>() + 2 * RAD + zm_ch<T>() - 1 + zm_ch<T>() - 1) / zm_ch<T>() * zm_ch<T>(); }
 template <typename T>
 constexpr int zm_pcols() { return zm_tx<T>() + zm_ch<T>(); }
-template <typename T>
-constexpr int zm_rows() { return zm_ty<T>() + 6; }
+template <typename T, int RAD>
+constexpr int zm_rows() { return zm_ty<T>() + 2 * RAD; }
 struct TmapSet {
   CUtensorMap halo[NF];  // fields of the state read with the stencil
   CUtensorMap prev[NF];  // fields of the other state (f_{k-1}, read pointwise)
 };
-template <typename T>
+template <typename T, int RAD>
 bool zmarch_supported(const Geom& g, const Region& r);
-template <typename T>
+template <typename T, int RAD>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
                    const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm = nullptr);
 

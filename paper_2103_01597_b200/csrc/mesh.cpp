@@ -76,7 +76,8 @@ int rank_of_xyz(const int c[3]) {
 mhd_status check_info(const mhd_mesh_info* info) {
   if (!info) return fail(MHD_EINVAL, "info is null");
   if (info->abi_version != MHD_ABI_VERSION) return fail(MHD_EUNSUPPORTED, "ABI version mismatch");
-  if (info->radius != MHD_RADIUS) return fail(MHD_EUNSUPPORTED, "only radius 3 (6th order) is built");
+  if (info->radius < 1 || info->radius > 4)
+    return fail(MHD_EUNSUPPORTED, "radius must be 1..4 (orders 2, 4, 6, 8; P:829-830)");
   if (info->dtype != MHD_F32 && info->dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "dtype must be F32 or F64");
   if (info->nranks < 1 || (info->nranks & (info->nranks - 1)) != 0)
     return fail(MHD_EDECOMP, "nranks must be a power of two (Morton partition, P:557)");
@@ -89,7 +90,7 @@ mhd_status check_info(const mhd_mesh_info* info) {
   partition_xyz(info->nranks, P);
   for (int a = 0; a < 3; ++a) {
     if (info->n[a] % P[a] != 0) return fail(MHD_EDECOMP, "p_i does not divide n_i (P:207)");
-    if (info->n[a] / P[a] <= 2 * MHD_RADIUS) return fail(MHD_ESMALL, "local extent n'_i <= 2r (P:705)");
+    if (info->n[a] / P[a] <= 2 * info->radius) return fail(MHD_ESMALL, "local extent n'_i <= 2r (P:705)");
   }
   return MHD_OK;
 }
@@ -106,6 +107,7 @@ std::vector<SegInfo> build_segments(const mhd_mesh_info* info, int rank) {
   coord_xyz(rank, c);
   int64_t n[3];
   for (int a = 0; a < 3; ++a) n[a] = info->n[a] / P[a];
+  const int rad = info->radius;
   std::vector<SegInfo> out;
   for (int kind = 1; kind <= 3; ++kind) {
     if (kind == 3 && !info->exchange_corners) continue;
@@ -123,9 +125,9 @@ std::vector<SegInfo> build_segments(const mhd_mesh_info* info, int rank) {
             s.offset[a] = o[a];
             // halo cells at offset o (receiver side) and the interior cells that fill them
             // (sender side): s' = ((s - r) mod n') + r, in interior coordinates
-            s.dst_first[a] = o[a] < 0 ? -MHD_RADIUS : (o[a] == 0 ? 0 : (int)n[a]);
-            s.src_first[a] = o[a] < 0 ? (int)n[a] - MHD_RADIUS : 0;
-            s.extent[a] = o[a] == 0 ? (int)n[a] : MHD_RADIUS;
+            s.dst_first[a] = o[a] < 0 ? -rad : (o[a] == 0 ? 0 : (int)n[a]);
+            s.src_first[a] = o[a] < 0 ? (int)n[a] - rad : 0;
+            s.extent[a] = o[a] == 0 ? (int)n[a] : rad;
             rc[a] = ((c[a] + o[a]) % P[a] + P[a]) % P[a];
             sc[a] = ((c[a] - o[a]) % P[a] + P[a]) % P[a];
           }
@@ -152,13 +154,20 @@ std::vector<SegInfo> build_segments(const mhd_mesh_info* info, int rank) {
 template <typename T>
 Coef<T> make_coef(const mhd_mesh_info& info, int k, double dt) {
   Coef<T> C;
-  const double c[3] = {3.0 / 4.0, -3.0 / 20.0, 1.0 / 60.0};
-  const double d[3] = {3.0 / 2.0, -3.0 / 20.0, 1.0 / 90.0};
-  const double c0 = -49.0 / 18.0;
-  const double e[3] = {270.0 / 720.0, -27.0 / 720.0, 2.0 / 720.0};
+  memset(&C, 0, sizeof(C));
+  // central differences of order 2r, i = 1..r (readings R#1, R#2); e_i = d_i / 4
+  static const double CW[5][4] = {{0}, {1.0 / 2.0}, {2.0 / 3.0, -1.0 / 12.0}, {3.0 / 4.0, -3.0 / 20.0, 1.0 / 60.0},
+                                  {4.0 / 5.0, -1.0 / 5.0, 4.0 / 105.0, -1.0 / 280.0}};
+  static const double DW[5][4] = {{0}, {1.0}, {4.0 / 3.0, -1.0 / 12.0}, {3.0 / 2.0, -3.0 / 20.0, 1.0 / 90.0},
+                                  {8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0}};
+  static const double C0[5] = {0, -2.0, -5.0 / 2.0, -49.0 / 18.0, -205.0 / 72.0};
+  const int rad = info.radius;
+  const double* c = CW[rad];
+  const double* d = DW[rad];
+  const double c0 = C0[rad];
   const double* ds = info.ds;
   for (int a = 0; a < 3; ++a) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < rad; ++i) {
       C.c1[a][i] = (T)(c[i] / ds[a]);
       C.d2[a][i] = (T)(d[i] / (ds[a] * ds[a]));
     }
@@ -166,7 +175,7 @@ Coef<T> make_coef(const mhd_mesh_info& info, int k, double dt) {
   }
   const int pa[3] = {0, 0, 1}, pb[3] = {1, 2, 2};
   for (int p = 0; p < 3; ++p)
-    for (int i = 0; i < 3; ++i) C.xw[p][i] = (T)(e[i] / (ds[pa[p]] * ds[pb[p]]));
+    for (int i = 0; i < rad; ++i) C.xw[p][i] = (T)(d[i] / 4.0 / (ds[pa[p]] * ds[pb[p]]));
   const mhd_params& ph = info.phys;
   C.gamma_cp = (T)(ph.gamma / ph.cp);
   C.gm1 = (T)(ph.gamma - 1.0);
@@ -212,11 +221,12 @@ Layout make_layout(const mhd_mesh_info* info, int rank, const std::vector<SegInf
   const int64_t al = 128 / (int64_t)es;
   for (int a = 0; a < 3; ++a) L.n[a] = info->n[a] / P[a];
   L.xo = al;
-  L.sy = (int64_t)align_up((size_t)(L.xo + L.n[0] + MHD_RADIUS + 1), (size_t)al);
-  L.sz = L.sy * (L.n[1] + 2 * MHD_RADIUS);
+  const int rad = info->radius;
+  L.sy = (int64_t)align_up((size_t)(L.xo + L.n[0] + rad + 1), (size_t)al);
+  L.sz = L.sy * (L.n[1] + 2 * rad);
   // + one row and a chunk of slack: tiled kernels may over-read (never use) past the last halo row
-  L.field_elems = (int64_t)align_up((size_t)(L.sz * (L.n[2] + 2 * MHD_RADIUS) + L.sy + 4 * al), (size_t)(256 / es));
-  L.origin = MHD_RADIUS * L.sz + MHD_RADIUS * L.sy + L.xo;
+  L.field_elems = (int64_t)align_up((size_t)(L.sz * (L.n[2] + 2 * rad) + L.sy + 4 * al), (size_t)(256 / es));
+  L.origin = rad * L.sz + rad * L.sy + L.xo;
   L.field_bytes = (size_t)L.field_elems * es;
   size_t off = 0;
   for (int s = 0; s < 2; ++s) {
@@ -373,11 +383,20 @@ mhd_status encode_tmaps(mhd_mesh* m) {
   }
   const bool f64 = m->info.dtype == MHD_F64;
   const size_t es = (size_t)m->info.dtype;
-  const cuuint64_t dims[3] = {(cuuint64_t)m->L.sy, (cuuint64_t)(m->g.ny + 2 * MHD_RADIUS),
-                              (cuuint64_t)(m->g.nz + 2 * MHD_RADIUS)};
+  const int rad = m->info.radius;
+  const cuuint64_t dims[3] = {(cuuint64_t)m->L.sy, (cuuint64_t)(m->g.ny + 2 * rad), (cuuint64_t)(m->g.nz + 2 * rad)};
   const cuuint64_t strides[2] = {(cuuint64_t)(m->L.sy * es), (cuuint64_t)(m->L.sz * es)};
-  const cuuint32_t halo_box[3] = {(cuuint32_t)(f64 ? zm_cols<double>() : zm_cols<float>()),
-                                  (cuuint32_t)(f64 ? zm_rows<double>() : zm_rows<float>()), 1};
+  int cols = 0, rows = 0;
+  switch (rad) {
+#define B2_BOX(RR)                                                             \
+  case RR:                                                                     \
+    cols = f64 ? zm_cols<double, RR>() : zm_cols<float, RR>();                 \
+    rows = f64 ? zm_rows<double, RR>() : zm_rows<float, RR>();                 \
+    break;
+    B2_BOX(1) B2_BOX(2) B2_BOX(3) B2_BOX(4)
+#undef B2_BOX
+  }
+  const cuuint32_t halo_box[3] = {(cuuint32_t)cols, (cuuint32_t)rows, 1};
   const cuuint32_t prev_box[3] = {(cuuint32_t)(f64 ? zm_pcols<double>() : zm_pcols<float>()),
                                   (cuuint32_t)(f64 ? zm_ty<double>() : zm_ty<float>()), 1};
   const cuuint32_t estr[3] = {1, 1, 1};
@@ -425,20 +444,41 @@ double seg_bytes(const SegList& L, size_t es) {
   return c * NF * (double)es * 2.0;
 }
 
-// The update of one region of the subdomain.
-template <typename T>
-void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out, const RemoteMap<T>* rm = nullptr) {
-  if (r.ext[0] <= 0 || r.ext[1] <= 0 || r.ext[2] <= 0) return;
+// The update of one region of the subdomain, with the kernels of the mesh's stencil radius.
+template <typename T, int RAD>
+void update_region_r(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out, const RemoteMap<T>* rm) {
   const Fields<T> in = m->fields<T>(m->cur), out = m->fields<T>(1 - m->cur);
   const Coef<T> C = make_coef<T>(m->info, k, dt);
-  const bool zm = m->variant != 1 && m->tmaps_ok && zmarch_supported<T>(m->g, r);
+  const bool zm = m->variant != 1 && m->tmaps_ok && zmarch_supported<T, RAD>(m->g, r);
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
   PhaseTimer t(m, m->stream, MHD_PHASE_UPDATE, cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
   if (zm)
-    launch_zmarch<T>(m->stream, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, rm);
+    launch_zmarch<T, RAD>(m->stream, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, rm);
   else
-    launch_direct<T>(m->stream, in, out, m->g, r, C, k, rhs_out, rm);
+    launch_direct<T, RAD>(m->stream, in, out, m->g, r, C, k, rhs_out, rm);
   m->launches++;
+}
+
+template <typename T>
+void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out, const RemoteMap<T>* rm = nullptr) {
+  if (r.ext[0] <= 0 || r.ext[1] <= 0 || r.ext[2] <= 0) return;
+  switch (m->info.radius) {
+    case 1: update_region_r<T, 1>(m, r, k, dt, rhs_out, rm); break;
+    case 2: update_region_r<T, 2>(m, r, k, dt, rhs_out, rm); break;
+    case 3: update_region_r<T, 3>(m, r, k, dt, rhs_out, rm); break;
+    case 4: update_region_r<T, 4>(m, r, k, dt, rhs_out, rm); break;
+  }
+}
+
+template <typename T>
+bool zmarch_ok(const mhd_mesh* m, const Region& r) {
+  switch (m->info.radius) {
+    case 1: return zmarch_supported<T, 1>(m->g, r);
+    case 2: return zmarch_supported<T, 2>(m->g, r);
+    case 3: return zmarch_supported<T, 3>(m->g, r);
+    case 4: return zmarch_supported<T, 4>(m->g, r);
+  }
+  return false;
 }
 
 template <typename T>
@@ -493,7 +533,7 @@ void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer,
   int thick[3];
   for (int a = 0; a < 3; ++a) {
     split[a] = m->P[a] > 1;
-    thick[a] = std::max(MHD_RADIUS, std::min(thick_in[a], n[a] / 2));
+    thick[a] = std::max(m->info.radius, std::min(thick_in[a], n[a] / 2));
     inner.lo[a] = split[a] ? thick[a] : 0;
     inner.ext[a] = split[a] ? n[a] - 2 * thick[a] : n[a];
   }
@@ -569,7 +609,7 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   if (st != MHD_OK) return st;
   Region inner;
   std::vector<Region> outer;
-  const int thick[3] = {MHD_RADIUS, MHD_RADIUS, MHD_RADIUS};
+  const int thick[3] = {m->info.radius, m->info.radius, m->info.radius};
   split_regions(m, inner, outer, thick);
   update_region<T>(m, inner, k, dt, rhs_out);
   st = halo_end<T>(m);
@@ -591,7 +631,7 @@ mhd_status load_impl(mhd_mesh* m, int field, const void* src, int src_dtype, int
     cudaMemcpy3DParms p;
     memset(&p, 0, sizeof(p));
     p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), (size_t)m->g.nx * es, (size_t)m->g.nx, (size_t)m->g.ny);
-    p.dstPtr = make_cudaPitchedPtr(origin, (size_t)m->g.sy * es, (size_t)m->g.sy, (size_t)(m->g.ny + 2 * MHD_RADIUS));
+    p.dstPtr = make_cudaPitchedPtr(origin, (size_t)m->g.sy * es, (size_t)m->g.sy, (size_t)(m->g.ny + 2 * m->info.radius));
     p.extent = make_cudaExtent((size_t)m->g.nx * es, (size_t)m->g.ny, (size_t)m->g.nz);
     p.kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CU(cudaMemcpy3DAsync(&p, m->stream));
@@ -622,7 +662,7 @@ mhd_status store_impl(mhd_mesh* m, int field, void* dst, int dst_dtype, int on_d
     cudaMemcpy3DParms p;
     memset(&p, 0, sizeof(p));
     p.srcPtr = make_cudaPitchedPtr(const_cast<TM*>(origin), (size_t)m->g.sy * es, (size_t)m->g.sy,
-                                   (size_t)(m->g.ny + 2 * MHD_RADIUS));
+                                   (size_t)(m->g.ny + 2 * m->info.radius));
     p.dstPtr = make_cudaPitchedPtr(dst, (size_t)m->g.nx * es, (size_t)m->g.nx, (size_t)m->g.ny);
     p.extent = make_cudaExtent((size_t)m->g.nx * es, (size_t)m->g.ny, (size_t)m->g.nz);
     p.kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -832,9 +872,10 @@ mhd_status mhd_store_grid(mhd_mesh* m, int32_t field, void* dst, int32_t on_devi
   if (!m || !dst || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad store_grid argument");
   const size_t es = (size_t)m->info.dtype;
   const char* base = m->ws + m->L.state_off[m->cur] + (size_t)field * m->L.field_bytes;
-  const char* first = base + (size_t)(m->L.xo - MHD_RADIUS) * es;  // (x, y, z) = (-3, -3, -3)
-  const size_t mx = (size_t)m->g.nx + 2 * MHD_RADIUS, my = (size_t)m->g.ny + 2 * MHD_RADIUS;
-  const size_t mz = (size_t)m->g.nz + 2 * MHD_RADIUS;
+  const int rad = m->info.radius;
+  const char* first = base + (size_t)(m->L.xo - rad) * es;  // (x, y, z) = (-r, -r, -r)
+  const size_t mx = (size_t)m->g.nx + 2 * rad, my = (size_t)m->g.ny + 2 * rad;
+  const size_t mz = (size_t)m->g.nz + 2 * rad;
   CU(cudaMemcpy2DAsync(dst, mx * es, first, (size_t)m->g.sy * es, mx * es, my * mz,
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, m->stream));
   if (!on_device) CU(cudaStreamSynchronize(m->stream));
@@ -934,8 +975,7 @@ mhd_status mhd_set_kernel(mhd_mesh* m, int32_t variant) {
   if (!m || variant < 0 || variant > 2) return fail(MHD_EINVAL, "variant must be 0, 1 or 2");
   if (variant == 2) {
     Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
-    const bool ok = m->tmaps_ok && (m->info.dtype == MHD_F64 ? zmarch_supported<double>(m->g, full)
-                                                            : zmarch_supported<float>(m->g, full));
+    const bool ok = m->tmaps_ok && (m->info.dtype == MHD_F64 ? zmarch_ok<double>(m, full) : zmarch_ok<float>(m, full));
     if (!ok) return fail(MHD_EUNSUPPORTED, "z-marching kernel does not support this geometry");
   }
   m->variant = variant;

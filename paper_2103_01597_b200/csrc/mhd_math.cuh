@@ -12,19 +12,20 @@
 
 namespace b2 {
 
-constexpr int R = 3;   // stencil radius (Eq. 1); 6th order, k = 2r
+constexpr int R = 3;     // default stencil radius (Eq. 1); 6th order, k = 2r
+constexpr int RMAX = 4;  // orders 2, 4, 6, 8
 constexpr int NF = 8;  // lnrho, ux, uy, uz, s, Ax, Ay, Az (Table B.1; order R#14)
 enum { LNRHO = 0, UX = 1, UY = 2, UZ = 3, SS = 4, AX = 5, AY = 6, AZ = 7 };
 
 // Coefficients of one mesh, passed by value as a kernel parameter.
-// Stencil weights (readings R#1, R#2) are pre-divided by the grid spacing.
+// Stencil weights (readings R#1, R#2) of order 2r are pre-divided by the grid spacing; at r = 3:
+// c = (3/4, -3/20, 1/60), d = (3/2, -3/20, 1/90), centre -49/18, e = d / 4 = (270, -27, 2)/720.
 template <typename T>
 struct Coef {
-  T c1[3][3];  // [axis][i-1]: first derivative  c_i / ds_a,          c = (3/4, -3/20, 1/60)
-  T d2[3][3];  // [axis][i-1]: second derivative d_i / ds_a^2,        d = (3/2, -3/20, 1/90)
-  T d0[3];     // [axis]:      centre weight    -49/18 / ds_a^2
-  T xw[3][3];  // [pair][i-1]: cross derivative e_i / (ds_a ds_b),     e = (270, -27, 2)/720
-               //              pairs 0 = (x,y), 1 = (x,z), 2 = (y,z)
+  T c1[3][RMAX];  // [axis][i-1]: first derivative  c_i / ds_a
+  T d2[3][RMAX];  // [axis][i-1]: second derivative d_i / ds_a^2
+  T d0[3];        // [axis]:      centre weight    c_0 / ds_a^2
+  T xw[3][RMAX];  // [pair][i-1]: cross derivative e_i / (ds_a ds_b); pairs 0 = (x,y), 1 = (x,z), 2 = (y,z)
   // physics (Table B.2; EOS reading R#5, conduction R#6)
   T gamma_cp, gm1, inv_cp, lnrho0, cs0sq, inv_T0, H_C, eta_inv_mu0, inv_mu0, nu, nu3, two_nu, zeta, eta, K;
   // RK3 update: f_{k+1} = f_k + rkA[k] (f_k - f_{k-1}) + rkB[k] RHS  (R#3, R#4)
@@ -52,47 +53,58 @@ template <> __device__ __forceinline__ double exp_<double>(double x) { return ex
 template <> __device__ __forceinline__ float exp_<float>(float x) { return expf(x); }
 
 // ---- canonical operator forms -------------------------------------------------------------
-// D1 along an axis from the differences  Dl_i = f(+i) - f(-i)
-template <typename T>
-__device__ __forceinline__ T d1_of(T dl1, T dl2, T dl3, const T* c) {
-  return fma_(c[2], dl3, fma_(c[1], dl2, c[0] * dl1));
+// D1 along an axis from the differences  Dl_i = f(+i) - f(-i), i = 1..RAD
+template <typename T, int RAD>
+__device__ __forceinline__ T d1_of(const T (&dl)[RAD], const T* c) {
+  T acc = c[0] * dl[0];
+#pragma unroll
+  for (int i = 1; i < RAD; ++i) acc = fma_(c[i], dl[i], acc);
+  return acc;
 }
 // D2 along an axis from the sums  Sg_i = f(+i) + f(-i)  and the centre value
-template <typename T>
-__device__ __forceinline__ T d2_of(T f0, T sg1, T sg2, T sg3, const T* d, T d0) {
-  return fma_(d[2], sg3, fma_(d[1], sg2, fma_(d[0], sg1, d0 * f0)));
+template <typename T, int RAD>
+__device__ __forceinline__ T d2_of(T f0, const T (&sg)[RAD], const T* d, T d0) {
+  T acc = d0 * f0;
+#pragma unroll
+  for (int i = 0; i < RAD; ++i) acc = fma_(d[i], sg[i], acc);
+  return acc;
 }
 
 // Accessor-driven gather of every derivative, in the canonical order.
 // V(q, dx, dy, dz) returns field q at the cell offset (dx, dy, dz).
 //
 // Cross derivatives (reading R#2; Eq. 14 point set):
-//   d_a d_b f = sum_{k=-3..3, k!=0} sgn(k) e_|k| / (ds_a ds_b) * Dl^a_|k|(f at +k e_b),
+//   d_a d_b f = sum_{k=-r..r, k!=0} sgn(k) e_|k| / (ds_a ds_b) * Dl^a_|k|(f at +k e_b),
 // accumulated in increasing k (the z-marching kernel accumulates plane by plane in this
 // same order).  The graddiv cross parts are
 //   x_0 = d_x d_z v_z  (+ d_x d_y v_y inserted at k = 0)
 //   x_1 = d_y d_z v_z  (+ d_x d_y v_x inserted at k = 0)
 //   x_2 = d_x d_z v_x and d_y d_z v_y interleaved per k.
-template <typename T, class Acc>
+template <typename T, int RAD, class Acc>
 __device__ __forceinline__ void axis_pair(const Acc& V, int q, int a, const Coef<T>& C, T f0, T& d1, T& d2) {
   const int ox = a == 0, oy = a == 1, oz = a == 2;
-  T p1 = V(q, ox, oy, oz), m1 = V(q, -ox, -oy, -oz);
-  T p2 = V(q, 2 * ox, 2 * oy, 2 * oz), m2 = V(q, -2 * ox, -2 * oy, -2 * oz);
-  T p3 = V(q, 3 * ox, 3 * oy, 3 * oz), m3 = V(q, -3 * ox, -3 * oy, -3 * oz);
-  d1 = d1_of(p1 - m1, p2 - m2, p3 - m3, C.c1[a]);
-  d2 = d2_of(f0, p1 + m1, p2 + m2, p3 + m3, C.d2[a], C.d0[a]);
+  T dl[RAD], sg[RAD];
+#pragma unroll
+  for (int i = 1; i <= RAD; ++i) {
+    const T p = V(q, i * ox, i * oy, i * oz), m = V(q, -i * ox, -i * oy, -i * oz);
+    dl[i - 1] = p - m;
+    sg[i - 1] = p + m;
+  }
+  d1 = d1_of<T, RAD>(dl, C.c1[a]);
+  d2 = d2_of<T, RAD>(f0, sg, C.d2[a], C.d0[a]);
 }
 
-// in-plane d_x d_y of field q (a = x, b = y)
-template <typename T, class Acc>
+// in-plane d_x d_y of field q (a = x, b = y), k = -r..r in increasing order
+template <typename T, int RAD, class Acc>
 __device__ __forceinline__ T cross_xy(const Acc& V, int q, const Coef<T>& C) {
   const T* w = C.xw[0];
-  T acc = (-w[2]) * (V(q, 3, -3, 0) - V(q, -3, -3, 0));
-  acc = fma_(-w[1], V(q, 2, -2, 0) - V(q, -2, -2, 0), acc);
-  acc = fma_(-w[0], V(q, 1, -1, 0) - V(q, -1, -1, 0), acc);
-  acc = fma_(w[0], V(q, 1, 1, 0) - V(q, -1, 1, 0), acc);
-  acc = fma_(w[1], V(q, 2, 2, 0) - V(q, -2, 2, 0), acc);
-  acc = fma_(w[2], V(q, 3, 3, 0) - V(q, -3, 3, 0), acc);
+  T acc = (-w[RAD - 1]) * (V(q, RAD, -RAD, 0) - V(q, -RAD, -RAD, 0));
+#pragma unroll
+  for (int k = -RAD + 1; k <= RAD; ++k) {
+    if (k == 0) continue;
+    const int i = k < 0 ? -k : k;
+    acc = fma_(k < 0 ? -w[i - 1] : w[i - 1], V(q, i, k, 0) - V(q, -i, k, 0), acc);
+  }
   return acc;
 }
 
@@ -107,16 +119,16 @@ __device__ __forceinline__ T zweight(const Coef<T>& C, int pair, int k) {
   return k < 0 ? -C.xw[pair][-k - 1] : C.xw[pair][k - 1];
 }
 
-template <typename T, class Acc>
+template <typename T, int RAD, class Acc>
 __device__ __forceinline__ void cross_parts(const Acc& V, int qx, int qy, int qz, const Coef<T>& C, T x[3]) {
-  const T P0 = cross_xy<T>(V, qy, C);  // d_x d_y v_y
-  const T P1 = cross_xy<T>(V, qx, C);  // d_x d_y v_x
-  T a0 = zweight(C, 1, -3) * zdelta<T>(V, qz, 0, -3);
-  T a1 = zweight(C, 2, -3) * zdelta<T>(V, qz, 1, -3);
-  T a2 = zweight(C, 1, -3) * zdelta<T>(V, qx, 0, -3);
-  a2 = fma_(zweight(C, 2, -3), zdelta<T>(V, qy, 1, -3), a2);
+  const T P0 = cross_xy<T, RAD>(V, qy, C);  // d_x d_y v_y
+  const T P1 = cross_xy<T, RAD>(V, qx, C);  // d_x d_y v_x
+  T a0 = zweight(C, 1, -RAD) * zdelta<T>(V, qz, 0, -RAD);
+  T a1 = zweight(C, 2, -RAD) * zdelta<T>(V, qz, 1, -RAD);
+  T a2 = zweight(C, 1, -RAD) * zdelta<T>(V, qx, 0, -RAD);
+  a2 = fma_(zweight(C, 2, -RAD), zdelta<T>(V, qy, 1, -RAD), a2);
 #pragma unroll
-  for (int k = -2; k <= 3; ++k) {
+  for (int k = -RAD + 1; k <= RAD; ++k) {
     if (k == 0) {
       a0 = a0 + P0;
       a1 = a1 + P1;
@@ -132,31 +144,31 @@ __device__ __forceinline__ void cross_parts(const Acc& V, int qx, int qy, int qz
   x[2] = a2;
 }
 
-template <typename T, class Acc>
+template <typename T, int RAD, class Acc>
 __device__ __forceinline__ void gather(const Acc& V, const Coef<T>& C, Derivs<T>& D) {
 #pragma unroll
   for (int q = 0; q < NF; ++q) D.f[q] = V(q, 0, 0, 0);
   // lnrho and s: first derivatives and Laplacian (axis points only)
   {
     T d2x, d2y, d2z;
-    axis_pair<T>(V, LNRHO, 0, C, D.f[LNRHO], D.gl[0], d2x);
-    axis_pair<T>(V, LNRHO, 1, C, D.f[LNRHO], D.gl[1], d2y);
-    axis_pair<T>(V, LNRHO, 2, C, D.f[LNRHO], D.gl[2], d2z);
+    axis_pair<T, RAD>(V, LNRHO, 0, C, D.f[LNRHO], D.gl[0], d2x);
+    axis_pair<T, RAD>(V, LNRHO, 1, C, D.f[LNRHO], D.gl[1], d2y);
+    axis_pair<T, RAD>(V, LNRHO, 2, C, D.f[LNRHO], D.gl[2], d2z);
     D.lapl = (d2x + d2y) + d2z;
-    axis_pair<T>(V, SS, 0, C, D.f[SS], D.gs[0], d2x);
-    axis_pair<T>(V, SS, 1, C, D.f[SS], D.gs[1], d2y);
-    axis_pair<T>(V, SS, 2, C, D.f[SS], D.gs[2], d2z);
+    axis_pair<T, RAD>(V, SS, 0, C, D.f[SS], D.gs[0], d2x);
+    axis_pair<T, RAD>(V, SS, 1, C, D.f[SS], D.gs[1], d2y);
+    axis_pair<T, RAD>(V, SS, 2, C, D.f[SS], D.gs[2], d2z);
     D.laps = (d2x + d2y) + d2z;
   }
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      axis_pair<T>(V, UX + i, a, C, D.f[UX + i], D.gu[i][a], D.d2u[i][a]);
-      axis_pair<T>(V, AX + i, a, C, D.f[AX + i], D.gA[i][a], D.d2A[i][a]);
+      axis_pair<T, RAD>(V, UX + i, a, C, D.f[UX + i], D.gu[i][a], D.d2u[i][a]);
+      axis_pair<T, RAD>(V, AX + i, a, C, D.f[AX + i], D.gA[i][a], D.d2A[i][a]);
     }
-  cross_parts<T>(V, UX, UY, UZ, C, D.xu);
-  cross_parts<T>(V, AX, AY, AZ, C, D.xA);
+  cross_parts<T, RAD>(V, UX, UY, UZ, C, D.xu);
+  cross_parts<T, RAD>(V, AX, AY, AZ, C, D.xA);
 }
 
 // ---- RHS of Eqs. B.1-B.4 -------------------------------------------------------

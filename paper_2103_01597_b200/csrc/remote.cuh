@@ -8,6 +8,7 @@
 // A cell (x, y, z) of the local interior belongs to the send region of segment o when,
 // per axis a:  o_a = +1 and x_a in [0, r);  o_a = -1 and x_a in [n_a - r, n_a);  or o_a = 0.
 // It lands in the receiver's halo at x_a + o_a n_a (s' = ((s - r) mod n') + r).
+// RAD is the stencil radius r.
 #pragma once
 #include "mhd_math.cuh"
 
@@ -22,12 +23,12 @@ struct RemoteMap {
 };
 
 // Store the 8 new values of cell (x, y, z) into every neighbour halo that holds a copy of it.
-template <typename T>
+template <typename T, int RAD>
 __device__ __forceinline__ void remote_store(const RemoteMap<T>& rm, int nx, int ny, int nz, long long sy,
                                              long long sz, int x, int y, int z, const T (&v)[NF]) {
-  const int sx = x < R ? 1 : (x >= nx - R ? -1 : 0);
-  const int syy = y < R ? 1 : (y >= ny - R ? -1 : 0);
-  const int szz = z < R ? 1 : (z >= nz - R ? -1 : 0);
+  const int sx = x < RAD ? 1 : (x >= nx - RAD ? -1 : 0);
+  const int syy = y < RAD ? 1 : (y >= ny - RAD ? -1 : 0);
+  const int szz = z < RAD ? 1 : (z >= nz - RAD ? -1 : 0);
   if ((sx | syy | szz) == 0) return;
 #pragma unroll
   for (int m = 1; m < 8; ++m) {

@@ -1,15 +1,16 @@
-// z-marching update kernel: the hot path on sm_100a.
+// z-marching update kernel: the hot path on sm_100a (template; instantiated per dtype and
+// stencil radius by zmarch_<dtype>_r<r>.cu).
 //
 // A CTA owns a TX x TY column of cells and marches it along z over a chunk of planes.
-//  * Staging: each plane (8 fields, tile + radius-3 halo in x and y) is fetched by TMA
-//    (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion) into a 5-slot
+//  * Staging: each plane (8 fields, tile + radius-r halo in x and y) is fetched by TMA
+//    (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion) into an (r + 2)-slot
 //    shared-memory ring, one plane ahead of the computation; f_{k-1} of the output plane
 //    (read pointwise by the RK3 update) rides in the same transaction.  One CTA barrier per
 //    plane protects slot reuse (a barrier-free variant with per-slot release counters measured
 //    3 % slower: profiles/r01/).
 //  * In-plane derivatives (x, y axes and the d_x d_y diagonals of Eq. 14) are read
 //    from the slot of the output plane o; the z column of every field comes from registers
-//    (planes o-3..o-1) and from the ring (o+1..o+3).
+//    (planes o-r..o-1) and from the ring (o+1..o+r).
 //  * The d_x d_z / d_y d_z cross terms are split: the k < 0 half is PUSHED from each plane into
 //    register accumulators of the next three outputs, reusing that plane's own x/y differences;
 //    the k > 0 half is PULLED from the ring.  This reproduces mhd_math.cuh::cross_parts term by
@@ -17,13 +18,13 @@
 //    (tests/test_gpu_parity.py::test_kernel_variants_bit_identical).
 //  * Fields are processed one vector at a time (A, then u, then lnrho and s) and the magnetic
 //    derivatives are contracted to B, mu0 j and lap A as soon as they exist, to keep the live
-//    register set small.  The march is unrolled by 3 so the register history rotates by
+//    register set small.  The march is unrolled by r so the register history rotates by
 //    renaming, not by moves.
+#pragma once
 #include "kernels.h"
 
 namespace b2 {
-
-namespace {
+namespace zm {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -52,18 +53,17 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-template <typename T, int TX, int TY>
+template <typename T, int RAD>
 struct ZCfg {
+  static constexpr int TX = zm_tx<T>(), TY = zm_ty<T>();
   static constexpr int ES = (int)sizeof(T);
-  static constexpr int COLS = zm_cols<T>();
-  static constexpr int ROWS = zm_rows<T>();
-  static_assert(TX == zm_tx<T>() && TY == zm_ty<T>(), "tile must match the TMA boxes");
+  static constexpr int COLS = zm_cols<T, RAD>();
+  static constexpr int ROWS = zm_rows<T, RAD>();
   static constexpr int FSZ = (ROWS * COLS * ES + 127) / 128 * 128 / ES;  // 128-B aligned TMA destinations
   static constexpr int SLOT = NF * FSZ;
-  // 5 slots: planes o..o+3 in use while o+4 streams in.  One CTA per SM (a 16x8 FP64 tile at two
-  // CTAs per SM and a 2-CTA FP32 variant both measured slower: profiles/r01/).
-  static constexpr int NSLOT = 5;
-  static constexpr int MINB = 1;
+  // r + 2 slots: planes o..o+r in use while o+r+1 streams in.  One CTA per SM (a 16x8 FP64 tile at
+  // two CTAs per SM and a 2-CTA FP32 variant both measured slower: profiles/r01/).
+  static constexpr int NSLOT = RAD + 2;
   static constexpr int NT = TX * TY;
   static constexpr int CH = zm_ch<T>();
   static constexpr int PCOLS = zm_pcols<T>();
@@ -71,25 +71,25 @@ struct ZCfg {
   static constexpr unsigned HALO_TX = (unsigned)(NF * ROWS * COLS * ES);
   static constexpr unsigned PREV_TX = (unsigned)(NF * TY * PCOLS * ES);
   static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128;
-  static constexpr unsigned NWARPS = (unsigned)(NT / 32);
+  static constexpr bool FITS = SMEM <= 227 * 1024;
 };
 
 // Register state carried along z by one thread.
-template <typename T>
+template <typename T, int RAD>
 struct March {
-  T hist[NF][3];   // physical storage of f(o-3), f(o-2), f(o-1); logical index j at phase PH is (j + PH) % 3
-  T acc[2][3][3];  // [u|A][logical output o, o+1, o+2 -> physical (j + PH) % 3][z-part of x_0, x_1, x_2]
+  T hist[NF][RAD];   // f(o-r) .. f(o-1); logical index j at phase PH lives at (j + PH) % r
+  T acc[2][RAD][3];  // [u|A][logical output o .. o+r-1 -> physical (j + PH) % r][z-part of x_0, x_1, x_2]
 };
 
-template <typename T, int TX, int TY, int MODE, bool REMOTE>
+template <typename T, int RAD, int MODE, bool REMOTE>
 struct ZStep {
-  using Z = ZCfg<T, TX, TY>;
+  using Z = ZCfg<T, RAD>;
   const T* ring;
   const T* prevbuf;
   const Coef<T>& C;
   int cell;   // offset of this thread's cell inside a field of a slot
   int pcell;  // offset inside a field of the f_{k-1} tile
-  int slot0;  // plane zb - 3 (first staged plane) has slot 0
+  int slot0;  // plane zb - r (first staged plane) has slot 0
   const RemoteMap<T>& rm;
 
   __device__ __forceinline__ const T* slot_of(int plane) const {
@@ -100,71 +100,79 @@ struct ZStep {
   }
 
   // x/y first and second derivatives of field q in the slot, with the differences kept
-  __device__ __forceinline__ void axis_xy(const T* sp, int q, T f0, T (&d1)[2], T (&d2)[2], T (&dlx)[3],
-                                          T (&dly)[3]) const {
-    T sg[2][3];
+  __device__ __forceinline__ void axis_xy(const T* sp, int q, T f0, T (&d1)[2], T (&d2)[2], T (&dlx)[RAD],
+                                          T (&dly)[RAD]) const {
+    T sgx[RAD], sgy[RAD];
 #pragma unroll
-    for (int i = 1; i <= 3; ++i) {
+    for (int i = 1; i <= RAD; ++i) {
       const T px = at(sp, q, i, 0), mx = at(sp, q, -i, 0);
       const T py = at(sp, q, 0, i), my = at(sp, q, 0, -i);
       dlx[i - 1] = px - mx;
-      sg[0][i - 1] = px + mx;
+      sgx[i - 1] = px + mx;
       dly[i - 1] = py - my;
-      sg[1][i - 1] = py + my;
+      sgy[i - 1] = py + my;
     }
-    d1[0] = d1_of(dlx[0], dlx[1], dlx[2], C.c1[0]);
-    d2[0] = d2_of(f0, sg[0][0], sg[0][1], sg[0][2], C.d2[0], C.d0[0]);
-    d1[1] = d1_of(dly[0], dly[1], dly[2], C.c1[1]);
-    d2[1] = d2_of(f0, sg[1][0], sg[1][1], sg[1][2], C.d2[1], C.d0[1]);
+    d1[0] = d1_of<T, RAD>(dlx, C.c1[0]);
+    d2[0] = d2_of<T, RAD>(f0, sgx, C.d2[0], C.d0[0]);
+    d1[1] = d1_of<T, RAD>(dly, C.c1[1]);
+    d2[1] = d2_of<T, RAD>(f0, sgy, C.d2[1], C.d0[1]);
   }
-  // z derivatives from the column
+  // z derivatives from the column: f(o+1..o+r) from the ring, f(o-r..o-1) from registers
   template <int PH>
-  __device__ __forceinline__ void axis_z(const March<T>& st, int q, T f0, T p1, T p2, T p3, T& d1, T& d2) const {
-    const T m1 = st.hist[q][(2 + PH) % 3], m2 = st.hist[q][(1 + PH) % 3], m3 = st.hist[q][(0 + PH) % 3];
-    d1 = d1_of(p1 - m1, p2 - m2, p3 - m3, C.c1[2]);
-    d2 = d2_of(f0, p1 + m1, p2 + m2, p3 + m3, C.d2[2], C.d0[2]);
+  __device__ __forceinline__ void axis_z(const March<T, RAD>& st, int q, T f0, const T* const (&sk)[RAD + 1], T& d1,
+                                         T& d2) const {
+    T dl[RAD], sg[RAD];
+#pragma unroll
+    for (int i = 1; i <= RAD; ++i) {
+      const T p = at(sk[i], q, 0, 0), m = st.hist[q][(RAD - i + PH) % RAD];
+      dl[i - 1] = p - m;
+      sg[i - 1] = p + m;
+    }
+    d1 = d1_of<T, RAD>(dl, C.c1[2]);
+    d2 = d2_of<T, RAD>(f0, sg, C.d2[2], C.d0[2]);
   }
   __device__ __forceinline__ T cross_xy_s(const T* sp, int q) const {
     const T* w = C.xw[0];
-    T a = (-w[2]) * (at(sp, q, 3, -3) - at(sp, q, -3, -3));
-    a = fma_(-w[1], at(sp, q, 2, -2) - at(sp, q, -2, -2), a);
-    a = fma_(-w[0], at(sp, q, 1, -1) - at(sp, q, -1, -1), a);
-    a = fma_(w[0], at(sp, q, 1, 1) - at(sp, q, -1, 1), a);
-    a = fma_(w[1], at(sp, q, 2, 2) - at(sp, q, -2, 2), a);
-    a = fma_(w[2], at(sp, q, 3, 3) - at(sp, q, -3, 3), a);
+    T a = (-w[RAD - 1]) * (at(sp, q, RAD, -RAD) - at(sp, q, -RAD, -RAD));
+#pragma unroll
+    for (int k = -RAD + 1; k <= RAD; ++k) {
+      if (k == 0) continue;
+      const int i = k < 0 ? -k : k;
+      a = fma_(k < 0 ? -w[i - 1] : w[i - 1], at(sp, q, i, k) - at(sp, q, -i, k), a);
+    }
     return a;
   }
-  // k < 0 half of the z-cross terms of plane p for vector v: outputs p+1 (k = -1), p+2 (k = -2),
-  // and a fresh accumulator for p+3 (k = -3), which lands in the physical slot of output p.
+  // k < 0 half of the z-cross terms of plane p for vector v: outputs p+j (k = -j, j < r) and a
+  // fresh accumulator for p+r (k = -r), which lands in the physical slot of output p.
   template <int PH>
-  __device__ __forceinline__ void push(March<T>& st, int v, const T (&dlx_x)[3], const T (&dly_y)[3],
-                                       const T (&dlx_z)[3], const T (&dly_z)[3]) const {
+  __device__ __forceinline__ void push(March<T, RAD>& st, int v, const T (&dlx_x)[RAD], const T (&dly_y)[RAD],
+                                       const T (&dlx_z)[RAD], const T (&dly_z)[RAD]) const {
     const T* wxz = C.xw[1];
     const T* wyz = C.xw[2];
 #pragma unroll
-    for (int j = 1; j <= 2; ++j) {
-      T* a = st.acc[v][(j + PH) % 3];
+    for (int j = 1; j < RAD; ++j) {
+      T* a = st.acc[v][(j + PH) % RAD];
       a[0] = fma_(-wxz[j - 1], dlx_z[j - 1], a[0]);
       a[1] = fma_(-wyz[j - 1], dly_z[j - 1], a[1]);
       a[2] = fma_(-wxz[j - 1], dlx_x[j - 1], a[2]);
       a[2] = fma_(-wyz[j - 1], dly_y[j - 1], a[2]);
     }
-    T* f = st.acc[v][(0 + PH) % 3];
-    f[0] = (-wxz[2]) * dlx_z[2];
-    f[1] = (-wyz[2]) * dly_z[2];
-    f[2] = fma_(-wyz[2], dly_y[2], (-wxz[2]) * dlx_x[2]);
+    T* f = st.acc[v][(0 + PH) % RAD];
+    f[0] = (-wxz[RAD - 1]) * dlx_z[RAD - 1];
+    f[1] = (-wyz[RAD - 1]) * dly_z[RAD - 1];
+    f[2] = fma_(-wyz[RAD - 1], dly_y[RAD - 1], (-wxz[RAD - 1]) * dlx_x[RAD - 1]);
   }
 
   // push-only pass over a plane below the chunk (prologue)
   template <int PH>
-  __device__ __forceinline__ void push_only(March<T>& st, int p) const {
+  __device__ __forceinline__ void push_only(March<T, RAD>& st, int p) const {
     const T* s0 = slot_of(p);
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const int qx = v == 0 ? UX : AX;
-      T dlx_x[3], dly_y[3], dlx_z[3], dly_z[3];
+      T dlx_x[RAD], dly_y[RAD], dlx_z[RAD], dly_z[RAD];
 #pragma unroll
-      for (int i = 1; i <= 3; ++i) {
+      for (int i = 1; i <= RAD; ++i) {
         dlx_x[i - 1] = at(s0, qx, i, 0) - at(s0, qx, -i, 0);
         dly_y[i - 1] = at(s0, qx + 1, 0, i) - at(s0, qx + 1, 0, -i);
         dlx_z[i - 1] = at(s0, qx + 2, i, 0) - at(s0, qx + 2, -i, 0);
@@ -173,17 +181,17 @@ struct ZStep {
       push<PH>(st, v, dlx_x, dly_y, dlx_z, dly_z);
     }
 #pragma unroll
-    for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % 3] = at(s0, q, 0, 0);
+    for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % RAD] = at(s0, q, 0, 0);
   }
 
   // Derivatives of one vector field (u or A) at output plane o: first and second derivatives
   // along every axis, the graddiv cross parts, and the push of plane o's differences.
   template <int PH>
-  __device__ __forceinline__ void vector_derivs(March<T>& st, int v, const T* s0, const T* s1, const T* s2,
-                                                const T* s3, T (&f)[3], T (&g)[3][3], T (&d2)[3][3],
-                                                T (&x)[3]) const {
+  __device__ __forceinline__ void vector_derivs(March<T, RAD>& st, int v, const T* const (&sk)[RAD + 1], T (&f)[3],
+                                                T (&g)[3][3], T (&d2)[3][3], T (&x)[3]) const {
     const int qx = v == 0 ? UX : AX;
-    T dlx[3][3], dly[3][3];
+    const T* s0 = sk[0];
+    T dlx[3][RAD], dly[3][RAD];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const int q = qx + c;
@@ -194,51 +202,50 @@ struct ZStep {
       g[c][1] = d1a[1];
       d2[c][0] = d2a[0];
       d2[c][1] = d2a[1];
-      axis_z<PH>(st, q, f[c], at(s1, q, 0, 0), at(s2, q, 0, 0), at(s3, q, 0, 0), g[c][2], d2[c][2]);
+      axis_z<PH>(st, q, f[c], sk, g[c][2], d2[c][2]);
     }
-    // graddiv cross parts: k < 0 (accumulated), + in-plane part at k = 0, then k = 1, 2, 3
+    // graddiv cross parts: k < 0 (accumulated), + in-plane part at k = 0, then k = 1..r
     const T P0 = cross_xy_s(s0, qx + 1);  // d_x d_y v_y
     const T P1 = cross_xy_s(s0, qx);      // d_x d_y v_x
-    const T* a = st.acc[v][(0 + PH) % 3];
+    const T* a = st.acc[v][(0 + PH) % RAD];
     x[0] = a[0] + P0;
     x[1] = a[1] + P1;
     x[2] = a[2];
     const T* wxz = C.xw[1];
     const T* wyz = C.xw[2];
 #pragma unroll
-    for (int kk = 1; kk <= 3; ++kk) {
-      const T* sk = kk == 1 ? s1 : (kk == 2 ? s2 : s3);
-      x[0] = fma_(wxz[kk - 1], at(sk, qx + 2, kk, 0) - at(sk, qx + 2, -kk, 0), x[0]);
-      x[1] = fma_(wyz[kk - 1], at(sk, qx + 2, 0, kk) - at(sk, qx + 2, 0, -kk), x[1]);
-      x[2] = fma_(wxz[kk - 1], at(sk, qx, kk, 0) - at(sk, qx, -kk, 0), x[2]);
-      x[2] = fma_(wyz[kk - 1], at(sk, qx + 1, 0, kk) - at(sk, qx + 1, 0, -kk), x[2]);
+    for (int kk = 1; kk <= RAD; ++kk) {
+      const T* s = sk[kk];
+      x[0] = fma_(wxz[kk - 1], at(s, qx + 2, kk, 0) - at(s, qx + 2, -kk, 0), x[0]);
+      x[1] = fma_(wyz[kk - 1], at(s, qx + 2, 0, kk) - at(s, qx + 2, 0, -kk), x[1]);
+      x[2] = fma_(wxz[kk - 1], at(s, qx, kk, 0) - at(s, qx, -kk, 0), x[2]);
+      x[2] = fma_(wyz[kk - 1], at(s, qx + 1, 0, kk) - at(s, qx + 1, 0, -kk), x[2]);
     }
     push<PH>(st, v, dlx[0], dly[1], dlx[2], dly[2]);
   }
 
   template <int PH>
-  __device__ __forceinline__ void full(March<T>& st, int o, const Fields<T>& out, const Geom& g, int k, bool active,
-                                       int x, int y, T* rhs_out) const {
-    const T* s0 = slot_of(o);
-    const T* s1 = slot_of(o + 1);
-    const T* s2 = slot_of(o + 2);
-    const T* s3 = slot_of(o + 3);
+  __device__ __forceinline__ void full(March<T, RAD>& st, int o, const Fields<T>& out, const Geom& g, int k,
+                                       bool active, int x, int y, T* rhs_out) const {
+    const T* sk[RAD + 1];
+#pragma unroll
+    for (int i = 0; i <= RAD; ++i) sk[i] = slot_of(o + i);
     // magnetic potential: derivatives, then B, mu0 j, lap A right away
     T fA[3], gA[3][3], d2A[3][3], xA[3];
-    vector_derivs<PH>(st, 1, s0, s1, s2, s3, fA, gA, d2A, xA);
+    vector_derivs<PH>(st, 1, sk, fA, gA, d2A, xA);
     const MagPart<T> m = mag_part<T>(gA, d2A, xA);
     // velocity
     T u[3], gu[3][3], d2u[3][3], xu[3];
-    vector_derivs<PH>(st, 0, s0, s1, s2, s3, u, gu, d2u, xu);
+    vector_derivs<PH>(st, 0, sk, u, gu, d2u, xu);
     // log density and entropy
     T sc[2], gsc[2][3], lap[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int q = h == 0 ? LNRHO : SS;
-      sc[h] = at(s0, q, 0, 0);
-      T d1a[2], d2a[2], dlx[3], dly[3], d2z;
-      axis_xy(s0, q, sc[h], d1a, d2a, dlx, dly);
-      axis_z<PH>(st, q, sc[h], at(s1, q, 0, 0), at(s2, q, 0, 0), at(s3, q, 0, 0), gsc[h][2], d2z);
+      sc[h] = at(sk[0], q, 0, 0);
+      T d1a[2], d2a[2], dlx[RAD], dly[RAD], d2z;
+      axis_xy(sk[0], q, sc[h], d1a, d2a, dlx, dly);
+      axis_z<PH>(st, q, sc[h], sk, gsc[h][2], d2z);
       gsc[h][0] = d1a[0];
       gsc[h][1] = d1a[1];
       lap[h] = (d2a[0] + d2a[1]) + d2z;
@@ -256,7 +263,7 @@ struct ZStep {
           fn[q] = rk_update<T>(k, fk[q], k > 0 ? pv[q * Z::PSZ] : (T)0, rhs[q], C);
           out.f[q][gidx] = fn[q];
         }
-        if (REMOTE) remote_store<T>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, o, fn);
+        if (REMOTE) remote_store<T, RAD>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, o, fn);
       } else {
         const long long n = (long long)g.nx * g.ny * g.nz;
         const long long li = ((long long)o * g.ny + y) * g.nx + x;
@@ -265,15 +272,24 @@ struct ZStep {
       }
     }
 #pragma unroll
-    for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % 3] = fk[q];
+    for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % RAD] = fk[q];
   }
 };
 
-template <typename T, int TX, int TY, int MODE, bool REMOTE>
-__global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
-    zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C, int k,
-                  T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm) {
-  using Z = ZCfg<T, TX, TY>;
+template <int N, int PH = 0, class F>
+__device__ __forceinline__ void unroll_phases(F&& f, int p, int ze) {
+  if constexpr (PH < N) {
+    if (p + PH < ze) f(std::integral_constant<int, PH>{}, p + PH);
+    unroll_phases<N, PH + 1>(f, p, ze);
+  }
+}
+
+template <typename T, int RAD, int MODE, bool REMOTE>
+__global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
+    zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C,
+                  int k, T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm) {
+  using Z = ZCfg<T, RAD>;
+  constexpr int TX = Z::TX, TY = Z::TY;
   // Dynamic shared memory starts at the (1024-B aligned) base of the CTA window (no static
   // shared memory in this kernel).  The pointer must stay visibly __shared__ so that the stencil
   // reads compile to LDS, not generic loads.
@@ -290,8 +306,8 @@ __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
   const int x = x0 + tx, y = y0 + ty;
   const bool active = x < r.lo[0] + r.ext[0] && y < r.lo[1] + r.ext[1];
   const bool need_prev = MODE == 0 && k > 0;
-  const int first = zb - 3;
-  const int xs = (x0 - 3) & ~(Z::CH - 1);  // 16-byte aligned box starts (interior origin is 128-B aligned)
+  const int first = zb - RAD;
+  const int xs = (x0 - RAD) & ~(Z::CH - 1);  // 16-byte aligned box starts (interior origin is 128-B aligned)
   const int pxs = x0 & ~(Z::CH - 1);
 
   if (tid == 0) {
@@ -301,19 +317,20 @@ __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
   }
   __syncthreads();
 
-  // one TMA transaction per staged plane P: its halo tile, plus f_{k-1} of output plane P - 3
+  // one TMA transaction per staged plane P: its halo tile, plus f_{k-1} of output plane P - r.
+  // Memory coordinates: the pitched field has a halo of r cells (element = interior + r in y, z).
   auto issue = [&](int P) {
     const int s = (P - first) % Z::NSLOT;
-    const int po = P - 3;
+    const int po = P - RAD;
     const bool pv = need_prev && po >= zb && po < ze;
     mbar_expect_tx(&mbar[s], Z::HALO_TX + (pv ? Z::PREV_TX : 0u));
     T* dst = ring + s * Z::SLOT;
 #pragma unroll
-    for (int q = 0; q < NF; ++q) tma_load_3d(dst + q * Z::FSZ, &tm.halo[q], &mbar[s], xs + xo, y0, P + 3);
+    for (int q = 0; q < NF; ++q) tma_load_3d(dst + q * Z::FSZ, &tm.halo[q], &mbar[s], xs + xo, y0, P + RAD);
     if (pv) {
       T* pd = prevbuf + (po & 1) * NF * Z::PSZ;
 #pragma unroll
-      for (int q = 0; q < NF; ++q) tma_load_3d(pd + q * Z::PSZ, &tm.prev[q], &mbar[s], pxs + xo, y0 + 3, po + 3);
+      for (int q = 0; q < NF; ++q) tma_load_3d(pd + q * Z::PSZ, &tm.prev[q], &mbar[s], pxs + xo, y0 + RAD, po + RAD);
     }
   };
   auto wait_plane = [&](int P) {
@@ -321,87 +338,81 @@ __global__ void __launch_bounds__(TX* TY, ZCfg<T, TX, TY>::MINB)
     mbar_wait(&mbar[rel % Z::NSLOT], (unsigned)((rel / Z::NSLOT) & 1));
   };
 
-  const ZStep<T, TX, TY, MODE, REMOTE> S{ring, prevbuf, C, (ty + R) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
-                                         first, rm};
-  March<T> st;
+  const ZStep<T, RAD, MODE, REMOTE> S{ring, prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
+                                      first, rm};
+  March<T, RAD> st;
 #pragma unroll
   for (int v = 0; v < 2; ++v)
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
+    for (int j = 0; j < RAD; ++j)
 #pragma unroll
       for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
 
   if (tid == 0)
-    for (int P = first; P <= zb && P <= ze + 2; ++P) issue(P);
-  wait_plane(first);
-  wait_plane(first + 1);
-  wait_plane(first + 2);
+    for (int P = first; P <= zb && P <= ze + RAD - 1; ++P) issue(P);
+#pragma unroll
+  for (int i = 0; i < RAD; ++i) wait_plane(first + i);
 
   auto iter = [&](auto ph, int p) {
     constexpr int PH = decltype(ph)::value;
     __syncthreads();  // every thread is done with iteration p - 1: its slot is refilled now
-    if (tid == 0 && p + 4 <= ze + 2) {
+    if (tid == 0 && p + RAD + 1 <= ze + RAD - 1) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(p + 4);
+      issue(p + RAD + 1);
     }
-    wait_plane(p + 3);  // plane p+3 and f_{k-1}(p) have landed
+    wait_plane(p + RAD);  // plane p+r and f_{k-1}(p) have landed
     if (p < zb)
       S.template push_only<PH>(st, p);
     else
       S.template full<PH>(st, p, out, g, k, active, x, y, rhs_out);
   };
 #pragma unroll 1
-  for (int p = first; p < ze; p += 3) {
-    iter(std::integral_constant<int, 0>{}, p);
-    if (p + 1 < ze) iter(std::integral_constant<int, 1>{}, p + 1);
-    if (p + 2 < ze) iter(std::integral_constant<int, 2>{}, p + 2);
-  }
+  for (int p = first; p < ze; p += RAD) unroll_phases<RAD>(iter, p, ze);
   if (REMOTE) __threadfence_system();  // peer halo stores visible before the completion signal
 }
 
 constexpr int kNZC = 64;
 
-template <typename T, int MODE, bool REMOTE>
+template <typename T, int RAD, int MODE, bool REMOTE>
 void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
                 const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm) {
-  constexpr int TXc = zm_tx<T>(), TYc = zm_ty<T>();
-  using Z = ZCfg<T, TXc, TYc>;
+  using Z = ZCfg<T, RAD>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(zmarch_kernel<T, TXc, TYc, MODE, REMOTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(zmarch_kernel<T, RAD, MODE, REMOTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Z::SMEM);
     attr = true;
   }
   const int nzc = r.ext[2] < kNZC ? r.ext[2] : kNZC;
-  dim3 grd((r.ext[0] + TXc - 1) / TXc, (r.ext[1] + TYc - 1) / TYc, (r.ext[2] + nzc - 1) / nzc);
-  zmarch_kernel<T, TXc, TYc, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm);
+  dim3 grd((r.ext[0] + Z::TX - 1) / Z::TX, (r.ext[1] + Z::TY - 1) / Z::TY, (r.ext[2] + nzc - 1) / nzc);
+  zmarch_kernel<T, RAD, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm);
 }
 
-}  // namespace
+}  // namespace zm
 
-template <typename T>
+template <typename T, int RAD>
 bool zmarch_supported(const Geom& g, const Region& r) {
   (void)g;
-  return r.ext[0] >= 16 && r.ext[1] >= 4 && r.ext[2] >= 1;
+  return zm::ZCfg<T, RAD>::FITS && r.ext[0] >= 16 && r.ext[1] >= 4 && r.ext[2] >= 1;
 }
 
-template <typename T>
+template <typename T, int RAD>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
                    const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm) {
-  RemoteMap<T> none;
-  if (rhs_out)
-    launch_cfg<T, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none);
-  else if (rm)
-    launch_cfg<T, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm);
-  else
-    launch_cfg<T, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none);
+  if constexpr (zm::ZCfg<T, RAD>::FITS) {
+    RemoteMap<T> none;
+    if (rhs_out)
+      zm::launch_cfg<T, RAD, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none);
+    else if (rm)
+      zm::launch_cfg<T, RAD, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm);
+    else
+      zm::launch_cfg<T, RAD, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none);
+  }
 }
 
-template bool zmarch_supported<float>(const Geom&, const Region&);
-template bool zmarch_supported<double>(const Geom&, const Region&);
-template void launch_zmarch<float>(cudaStream_t, const TmapSet&, const Fields<float>&, const Geom&, const Region&,
-                                   const Coef<float>&, int, float*, int, const RemoteMap<float>*);
-template void launch_zmarch<double>(cudaStream_t, const TmapSet&, const Fields<double>&, const Geom&, const Region&,
-                                    const Coef<double>&, int, double*, int, const RemoteMap<double>*);
+#define B2_ZMARCH_INSTANTIATE(T, RAD)                                                                      \
+  template bool zmarch_supported<T, RAD>(const Geom&, const Region&);                                       \
+  template void launch_zmarch<T, RAD>(cudaStream_t, const TmapSet&, const Fields<T>&, const Geom&, const Region&, \
+                                      const Coef<T>&, int, T*, int, const RemoteMap<T>*);
 
 }  // namespace b2

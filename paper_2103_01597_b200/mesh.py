@@ -26,7 +26,8 @@ class Mesh:
         self.torch = torch
         self.dtype = int(dtype)
         self.tdtype = getattr(torch, _TORCH_DT[self.dtype])
-        self.info = native.make_info(n_xyz, ds_xyz, params, dtype, rank, nranks, exchange_corners)
+        self.radius = int(radius)
+        self.info = native.make_info(n_xyz, ds_xyz, params, dtype, rank, nranks, exchange_corners, radius)
         self.nbytes = native.mhd_workspace_bytes(self.info)
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
@@ -86,8 +87,8 @@ class Mesh:
         return out
 
     def store_grid(self):
-        """Halo-inclusive local grids, (8, nz'+6, ny'+6, nx'+6), on the host (test hook)."""
-        sh = tuple(v + 6 for v in self.shape)
+        """Halo-inclusive local grids, (8, nz'+2r, ny'+2r, nx'+2r), on the host (test hook)."""
+        sh = tuple(v + 2 * self.radius for v in self.shape)
         out = self.torch.empty((8,) + sh, dtype=self.tdtype).pin_memory()
         for q in range(8):
             native.mhd_store_grid(self.handle, q, out[q].data_ptr(), False)

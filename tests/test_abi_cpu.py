@@ -68,10 +68,11 @@ def test_decompose_errors(n, nranks, status):
 def test_unsupported_radius_and_dtype():
     nat = _native()
     import ctypes
-    info = _info((32, 32, 32))
-    info.radius = 2
     b = ctypes.c_size_t()
-    assert nat.lib.mhd_workspace_bytes(ctypes.byref(info), ctypes.byref(b)) == 4
+    for r, st in ((0, 4), (5, 4), (1, 0), (2, 0), (3, 0), (4, 0)):
+        info = _info((32, 32, 32))
+        info.radius = r  # orders 2, 4, 6, 8 are built
+        assert nat.lib.mhd_workspace_bytes(ctypes.byref(info), ctypes.byref(b)) == st
     info = _info((32, 32, 32))
     info.dtype = 2
     assert nat.lib.mhd_workspace_bytes(ctypes.byref(info), ctypes.byref(b)) == 4
@@ -107,6 +108,18 @@ def test_segments_tile_the_halo(n, corners):
             assert np.all(shell == 1)
         else:
             assert np.all(shell <= 1) and (shell == 0).sum() == 216
+
+
+@pytest.mark.parametrize("r", [1, 2, 4])
+def test_segments_other_orders(r):
+    """Segment extents follow the radius: the halo of width r is tiled exactly (Eqs. 2-3)."""
+    nat = _native()
+    n = (20, 18, 16)
+    info = nat.make_info(n, (0.1,) * 3, synth.P0, exchange_corners=True, radius=r)
+    segs = nat.mhd_segment_table(info, 0)
+    total = sum(int(np.prod(s["extent"])) for s in segs)
+    assert total == (n[0] + 2 * r) * (n[1] + 2 * r) * (n[2] + 2 * r) - n[0] * n[1] * n[2]
+    assert all(e in (r, nv) for s in segs for e, nv in zip(s["extent"], n))
 
 
 def test_largest_segment_is_12MiB_at_256():

@@ -227,3 +227,65 @@ def test_full_size_256_rhs_and_substep():
     assert _field_err(got, ref) <= 1e-11
     assert _norm_err(got - st, ref - st) <= 1e-10
     m.close()
+
+
+# ---- stencil orders 2, 4, 6, 8 -------------------------------------------------------------
+@pytest.mark.parametrize("r", [1, 2, 3, 4])
+def test_orders_rhs_steps_and_kernels(r):
+    """Every order: RHS parity, 3 RK3 steps parity, and the direct and z-marching kernels agree
+    bit for bit (FP64 radius 4 runs on the direct kernel only: its ring does not fit in smem)."""
+    import paper_2103_01597_b200 as b2
+    from paper_2103_01597_b200 import MhdError
+    n = (40, 28, 24)
+    ds = synth.spacing(n)
+    st = synth.pcg64_state((n[2], n[1], n[0]))
+    outs = []
+    for variant in (1, 2):
+        m, _ = _mesh(n, ds, PSTRONG, radius=r)
+        try:
+            m.set_kernel(variant)
+        except MhdError:
+            assert variant == 2 and r == 4
+            m.close()
+            continue
+        m.load(st)
+        got = m.debug_rhs().cpu().numpy()
+        ref = oracle.rhs(st, ds, PSTRONG, r=r)
+        assert _norm_err(got, ref) <= 1e-12, (r, variant)
+        for _ in range(3):
+            m.step(1e-5)
+        outs.append(m.store().cpu().numpy())
+        m.close()
+    ref = oracle.integrate(st, ds, PSTRONG, 1e-5, 3, r=r)
+    for o in outs:
+        assert _field_err(o, ref) <= 1e-11
+        assert _norm_err(o - st, ref - st) <= 1e-9
+    if len(outs) == 2:
+        assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("r", [1, 4])
+def test_orders_halo_sentinel_bitwise(r):
+    n = (20, 18, 16)
+    m, _ = _mesh(n, radius=r, exchange_corners=True)
+    nz, ny, nx = n[2], n[1], n[0]
+    st = (np.arange(8)[:, None, None, None] * 1e6 + np.arange(nz * ny * nx).reshape(nz, ny, nx)).astype(np.float64)
+    m.load(st)
+    m.halo_exchange()
+    grid = m.store_grid().numpy()
+    expect = np.stack([oracle.periodic_fill(oracle.with_halo(st[q], r), r=r) for q in range(8)])
+    assert np.array_equal(grid, expect)
+    m.close()
+
+
+def test_order8_fp32_zmarch():
+    n = (40, 24, 20)
+    ds = synth.spacing(n)
+    m, _ = _mesh(n, ds, dtype=4, radius=4)
+    m.set_kernel(2)
+    st = synth.pcg64_state((n[2], n[1], n[0]), dtype=np.float32)
+    m.load(st)
+    got = m.debug_rhs().cpu().numpy().astype(np.float64)
+    ref = oracle.rhs(st.astype(np.float64), ds, synth.P0, r=4)
+    assert _norm_err(got, ref) <= 1e-4
+    m.close()

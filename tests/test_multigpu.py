@@ -15,9 +15,9 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _run(nproc, N, corners=0, steps=3, port=29511, exchange="p2p"):
+def _run(nproc, N, corners=0, steps=3, port=29511, exchange="p2p", radius=3):
     env = dict(os.environ, MGPU_N=",".join(map(str, N)), MGPU_CORNERS=str(corners), MGPU_STEPS=str(steps),
-               MGPU_EXCHANGE=exchange)
+               MGPU_EXCHANGE=exchange, MGPU_RADIUS=str(radius))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tools", "mgpu_check.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
@@ -33,4 +33,13 @@ def test_multigpu_halo_and_bit_identity(nproc, corners, exchange):
         pytest.skip(f"needs {nproc} GPUs")
     N = {2: (40, 36, 32), 4: (40, 32, 32), 8: (32, 32, 32)}[nproc]
     rc, out = _run(nproc, N, corners, port=29500 + nproc * 4 + corners * 2 + (exchange == "p2p"), exchange=exchange)
+    assert rc == 0, out[-4000:]
+
+
+@pytest.mark.parametrize("radius", [1, 2, 4])
+def test_multigpu_other_orders(radius):
+    """Orders 2, 4, 8 on 2 GPUs with the peer-memory exchange: bitwise halo, 1-vs-2 GPU identity."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    rc, out = _run(2, (40, 36, 32), 0, port=29560 + radius, exchange="p2p", radius=radius)
     assert rc == 0, out[-4000:]

@@ -35,12 +35,13 @@ def main():
     steps = int(os.environ.get("MGPU_STEPS", "3"))
     corners = bool(int(os.environ.get("MGPU_CORNERS", "0")))
     exchange = os.environ.get("MGPU_EXCHANGE", "p2p")
+    radius = int(os.environ.get("MGPU_RADIUS", "3"))
     ds = synth.spacing(N)
     res = {"rank": rank, "world": world, "N": N}
     ok = True
 
     mesh = b2.Mesh(N, ds, synth.P0, b2.MHD_F64, rank=rank, nranks=world, exchange_corners=corners,
-                   exchange=exchange)
+                   exchange=exchange, radius=radius)
     res["exchange"] = exchange
     Pz = tuple(reversed(mesh.P))
     cz = tuple(reversed(mesh.coord))
@@ -52,12 +53,12 @@ def main():
     mesh.load(np.ascontiguousarray(G.local_interior(glob, Pz, cz)))
     mesh.halo_exchange()
     grid = mesh.store_grid().numpy()
-    expect = G.local_subgrid_with_halo(glob, Pz, cz)
+    expect = G.local_subgrid_with_halo(glob, Pz, cz, r=radius)
     mask = np.ones(grid.shape[1:], bool)
     if not corners:
-        for zs in (slice(0, 3), slice(-3, None)):
-            for ys in (slice(0, 3), slice(-3, None)):
-                for xs in (slice(0, 3), slice(-3, None)):
+        for zs in (slice(0, radius), slice(-radius, None)):
+            for ys in (slice(0, radius), slice(-radius, None)):
+                for xs in (slice(0, radius), slice(-radius, None)):
                     mask[zs, ys, xs] = False
     res["halo_bitwise"] = bool(np.array_equal(grid[:, mask], expect[:, mask]))
     ok &= res["halo_bitwise"]
@@ -75,7 +76,7 @@ def main():
         for c, part in parts:
             n = part.shape[1:]
             full[:, c[0] * n[0]:(c[0] + 1) * n[0], c[1] * n[1]:(c[1] + 1) * n[1], c[2] * n[2]:(c[2] + 1) * n[2]] = part
-        single = b2.Mesh(N, ds, synth.P0, b2.MHD_F64)
+        single = b2.Mesh(N, ds, synth.P0, b2.MHD_F64, radius=radius)
         single.load(st)
         for _ in range(steps):
             single.step(synth.DT)
@@ -85,7 +86,7 @@ def main():
         ok &= res["bit_identical_vs_1gpu"]
         if os.environ.get("MGPU_ORACLE", "1") == "1":
             import oracle
-            ref = oracle.integrate(st, ds, synth.P0, synth.DT, steps)
+            ref = oracle.integrate(st, ds, synth.P0, synth.DT, steps, r=radius)
             e = max(float(np.max(np.abs(full[q] - ref[q]) / np.maximum(np.abs(ref[q]), 1e-3 * np.max(np.abs(ref[q])))))
                     for q in range(8))
             res["oracle_field_err"] = e
