@@ -102,9 +102,30 @@ void launch_remote_copy(cudaStream_t st, const Fields<T>& fl, const Geom& g, con
   remote_copy_kernel<T><<<L.nblocks, 256, 0, st>>>(fl, g, L, rm);
 }
 
-// Cross-GPU ordering with system-scope flags: after an operation that writes into the peers' halos
-// (or reads the local halo), each rank publishes its operation count into every neighbour's flag
-// slot; before the next such operation it waits until all neighbours published the previous count.
+// Cross-GPU ordering with system-scope flags.  Every operation that touches halos across ranks
+// (a boundary update that stores into the neighbours' halos, or a halo copy) has a sequence number
+// s and is bracketed by
+//   sync(s):  publish arrive = s to every neighbour (all earlier work of this rank on the stream,
+//             reads of its own halo included, is complete), then wait until every neighbour has
+//             arrive >= s (it is done reading what we are about to overwrite) and done >= s - 1
+//             (its writes into our halo from the previous operation have landed);
+//   done(s):  after the remote stores, fence and publish done = s.
+__global__ void p2p_sync_kernel(FlagSet peer_arrive, FlagSet my_arrive, FlagSet my_done, unsigned long long seq) {
+  for (int i = 0; i < peer_arrive.n; ++i)
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(peer_arrive.ptr[i]), "l"(seq) : "memory");
+  for (int i = 0; i < my_arrive.n; ++i) {
+    const long long t0 = clock64();
+    for (;;) {
+      unsigned long long a, d;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(a) : "l"(my_arrive.ptr[i]) : "memory");
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(d) : "l"(my_done.ptr[i]) : "memory");
+      if (a >= seq && d + 1 >= seq) break;
+      __nanosleep(128);
+      if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: a neighbour never arrived
+    }
+  }
+}
+
 __global__ void p2p_signal_kernel(FlagSet fs, unsigned long long seq) {
   __threadfence_system();
   for (int i = 0; i < fs.n; ++i)
@@ -119,11 +140,15 @@ __global__ void p2p_wait_kernel(FlagSet fs, unsigned long long seq) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(fs.ptr[i]) : "memory");
       if (v >= seq) break;
       __nanosleep(128);
-      if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: a neighbour never arrived
+      if (clock64() - t0 > 40000000000LL) __trap();
     }
   }
 }
 
+void launch_p2p_sync(cudaStream_t st, const FlagSet& peer_arrive, const FlagSet& my_arrive, const FlagSet& my_done,
+                     unsigned long long seq) {
+  p2p_sync_kernel<<<1, 1, 0, st>>>(peer_arrive, my_arrive, my_done, seq);
+}
 void launch_p2p_signal(cudaStream_t st, const FlagSet& fs, unsigned long long seq) {
   p2p_signal_kernel<<<1, 1, 0, st>>>(fs, seq);
 }

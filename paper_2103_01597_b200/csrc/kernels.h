@@ -57,6 +57,8 @@ struct FlagSet {
   int n;
 };
 void launch_p2p_signal(cudaStream_t st, const FlagSet& fs, unsigned long long seq);
+void launch_p2p_sync(cudaStream_t st, const FlagSet& peer_arrive, const FlagSet& my_arrive, const FlagSet& my_done,
+                     unsigned long long seq);
 void launch_p2p_wait(cudaStream_t st, const FlagSet& fs, unsigned long long seq);
 template <typename T>
 void launch_segments(cudaStream_t st, const Fields<T>& fl, const Geom& g, const SegList& L, int kind, T* buf);

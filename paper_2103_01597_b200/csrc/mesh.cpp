@@ -247,8 +247,8 @@ Layout make_layout(const mhd_mesh_info* info, int rank, const std::vector<SegInf
   off = align_up(off + (size_t)L.recv_cells * NF * es, 256);
   L.red_off = off;
   off = align_up(off + kReduceBlocks * kReduceVals * sizeof(double), 256);
-  L.flags_off = off;  // peer-memory exchange: one operation counter per rank, written by that rank
-  off = align_up(off + (size_t)info->nranks * sizeof(unsigned long long), 256);
+  L.flags_off = off;  // peer-memory exchange: arrive[nranks] then done[nranks], slot p written by rank p
+  off = align_up(off + 2 * (size_t)info->nranks * sizeof(unsigned long long), 256);
   L.total = off;
   return L;
 }
@@ -287,7 +287,7 @@ struct mhd_mesh {
   unsigned long long seq = 0;       // operations that touched halos across ranks
   bool halo_valid = false;          // halos of the current state already delivered by the last update
   SegList remote_list;              // remote segments with buf_off = peer slot (halo copy after a load)
-  FlagSet sig, wt;
+  FlagSet peer_arrive, peer_done, my_arrive, my_done;
   template <typename T>
   RemoteMap<T> remote_map(int dest_state) const {
     RemoteMap<T> rm;
@@ -564,10 +564,11 @@ void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer,
 // the neighbours proceed.
 template <typename T>
 void p2p_halo_copy(mhd_mesh* m) {
-  launch_p2p_wait(m->stream, m->wt, m->seq);
+  const unsigned long long s = ++m->seq;
+  launch_p2p_sync(m->stream, m->peer_arrive, m->my_arrive, m->my_done, s);
   const RemoteMap<T> rm = m->remote_map<T>(m->cur);
   launch_remote_copy<T>(m->stream, m->fields<T>(m->cur), m->g, m->remote_list, rm);
-  launch_p2p_signal(m->stream, m->sig, ++m->seq);
+  launch_p2p_signal(m->stream, m->peer_done, s);
   m->launches += 3;
   m->halo_valid = true;
 }
@@ -585,16 +586,17 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   std::vector<Region> outer;
   const int thick[3] = {zm_tx<T>(), zm_ty<T>(), 8};
   split_regions(m, inner, outer, thick);
+  const unsigned long long s = ++m->seq;
   {
     PhaseTimer t(m, m->stream, MHD_PHASE_EXCHANGE, 0.0);
-    launch_p2p_wait(m->stream, m->wt, m->seq);
+    launch_p2p_sync(m->stream, m->peer_arrive, m->my_arrive, m->my_done, s);
     m->launches++;
   }
   // boundary slabs: update + store into the neighbours' halos (the fused send), then publish;
   // the inner segment needs no remote halo and runs while the neighbours proceed
   const RemoteMap<T> rm = m->remote_map<T>(1 - m->cur);
   for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, rhs_out ? nullptr : &rm);
-  launch_p2p_signal(m->stream, m->sig, ++m->seq);
+  launch_p2p_signal(m->stream, m->peer_done, s);
   m->launches++;
   update_region<T>(m, inner, k, dt, rhs_out);
   if (!rhs_out) m->halo_valid = true;  // the neighbours are delivering the new state's halo
@@ -609,7 +611,9 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   if (st != MHD_OK) return st;
   Region inner;
   std::vector<Region> outer;
-  const int thick[3] = {m->info.radius, m->info.radius, m->info.radius};
+  // slabs one tile thick so that they run on the tiled kernel; the exchange stays hidden behind
+  // the (smaller) inner segment
+  const int thick[3] = {zm_tx<T>(), zm_ty<T>(), 8};
   split_regions(m, inner, outer, thick);
   update_region<T>(m, inner, k, dt, rhs_out);
   st = halo_end<T>(m);
@@ -892,7 +896,7 @@ mhd_status mhd_halo_exchange(mhd_mesh* m) {
       launch_segments<float>(m->stream, m->fields<float>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
       p2p_halo_copy<float>(m);
     }
-    launch_p2p_wait(m->stream, m->wt, m->seq);  // the neighbours' copies into this halo have landed
+    launch_p2p_wait(m->stream, m->my_done, m->seq);  // the neighbours' copies into this halo have landed
     m->launches += 2;
     CU(cudaGetLastError());
     return MHD_OK;
@@ -1039,12 +1043,18 @@ mhd_status mhd_p2p_open(mhd_mesh* m, const void* blobs) {
     m->ipc_bases.push_back(base);
     m->peer_ws[p.peer] = static_cast<char*>(base) + off;
   }
-  memset(&m->sig, 0, sizeof(m->sig));
-  memset(&m->wt, 0, sizeof(m->wt));
+  memset(&m->peer_arrive, 0, sizeof(FlagSet));
+  memset(&m->peer_done, 0, sizeof(FlagSet));
+  memset(&m->my_arrive, 0, sizeof(FlagSet));
+  memset(&m->my_done, 0, sizeof(FlagSet));
+  const int nr = m->info.nranks;
   for (auto& p : m->peers) {
-    m->sig.ptr[m->sig.n++] =
-        reinterpret_cast<unsigned long long*>(m->peer_ws[p.peer] + m->L.flags_off) + m->info.rank;
-    m->wt.ptr[m->wt.n++] = reinterpret_cast<unsigned long long*>(m->ws + m->L.flags_off) + p.peer;
+    unsigned long long* peer_flags = reinterpret_cast<unsigned long long*>(m->peer_ws[p.peer] + m->L.flags_off);
+    unsigned long long* my_flags = reinterpret_cast<unsigned long long*>(m->ws + m->L.flags_off);
+    m->peer_arrive.ptr[m->peer_arrive.n++] = peer_flags + m->info.rank;
+    m->peer_done.ptr[m->peer_done.n++] = peer_flags + nr + m->info.rank;
+    m->my_arrive.ptr[m->my_arrive.n++] = my_flags + p.peer;
+    m->my_done.ptr[m->my_done.n++] = my_flags + nr + p.peer;
   }
   // remote segments (buf_off = peer slot) for the halo copy of a freshly loaded state
   memset(&m->remote_list, 0, sizeof(m->remote_list));

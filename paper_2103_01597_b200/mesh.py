@@ -16,9 +16,10 @@ _TORCH_DT = {native.MHD_F64: "float64", native.MHD_F32: "float32"}
 class Mesh:
     def __init__(self, n_xyz, ds_xyz, params: dict, dtype: int = native.MHD_F64, rank: int = 0, nranks: int = 1,
                  exchange_corners: bool = False, stream=None, process_group=None, kernel: int = 0,
-                 exchange: str = "nccl"):
+                 exchange: str = "nccl", radius: int = 3):
         """exchange (nranks > 1): "p2p" = boundary results stored straight into the neighbours' halos
-        over NVLink (CUDA IPC peer memory); "nccl" = pack, NCCL send/recv, unpack."""
+        over NVLink (CUDA IPC peer memory); "nccl" = pack, NCCL send/recv, unpack.
+        radius: stencil radius r, order 2r = 2, 4, 6 (default, the paper's benchmarks) or 8."""
         import torch
 
         if not torch.cuda.is_available():
