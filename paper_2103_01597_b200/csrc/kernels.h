@@ -73,11 +73,12 @@ void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scra
 // TMA boxes per plane and field.  TMA requires the innermost start coordinate to be 16-byte
 // aligned, so boxes start at x rounded down to 16 bytes and are widened accordingly: halo box
 // COLS x ROWS x 1 from (floor16(x0 - r), y0 - r, z), f_{k-1} box PCOLS x TY x 1 from (floor16(x0), y0, z).
-// Tile of a CTA: 32 x 8 cells (a 16 x 8 FP64 tile at two CTAs per SM measured slower).
+// Tile of a CTA: 32 x 8 cells (a 16 x 8 FP64 tile at two CTAs per SM measured slower); 32 x 4
+// for FP64 at radius 4, whose (r + 2)-plane ring of 32 x 8 tiles would not fit in shared memory.
 template <typename T>
 constexpr int zm_tx() { return 32; }
-template <typename T>
-constexpr int zm_ty() { return 8; }
+template <typename T, int RAD = 3>
+constexpr int zm_ty() { return (sizeof(T) == 8 && RAD >= 4) ? 4 : 8; }
 template <typename T>
 constexpr int zm_ch() { return 16 / (int)sizeof(T); }
 template <typename T, int RAD>
@@ -85,7 +86,7 @@ constexpr int zm_cols() { return (zm_tx<T>() + 2 * RAD + zm_ch<T>() - 1 + zm_ch<
 template <typename T>
 constexpr int zm_pcols() { return zm_tx<T>() + zm_ch<T>(); }
 template <typename T, int RAD>
-constexpr int zm_rows() { return zm_ty<T>() + 2 * RAD; }
+constexpr int zm_rows() { return zm_ty<T, RAD>() + 2 * RAD; }
 struct TmapSet {
   CUtensorMap halo[NF];  // fields of the state read with the stencil
   CUtensorMap prev[NF];  // fields of the other state (f_{k-1}, read pointwise)

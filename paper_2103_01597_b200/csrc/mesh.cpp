@@ -386,19 +386,19 @@ mhd_status encode_tmaps(mhd_mesh* m) {
   const int rad = m->info.radius;
   const cuuint64_t dims[3] = {(cuuint64_t)m->L.sy, (cuuint64_t)(m->g.ny + 2 * rad), (cuuint64_t)(m->g.nz + 2 * rad)};
   const cuuint64_t strides[2] = {(cuuint64_t)(m->L.sy * es), (cuuint64_t)(m->L.sz * es)};
-  int cols = 0, rows = 0;
+  int cols = 0, rows = 0, pty = 0;
   switch (rad) {
 #define B2_BOX(RR)                                                             \
   case RR:                                                                     \
     cols = f64 ? zm_cols<double, RR>() : zm_cols<float, RR>();                 \
     rows = f64 ? zm_rows<double, RR>() : zm_rows<float, RR>();                 \
+    pty = f64 ? zm_ty<double, RR>() : zm_ty<float, RR>();                      \
     break;
     B2_BOX(1) B2_BOX(2) B2_BOX(3) B2_BOX(4)
 #undef B2_BOX
   }
   const cuuint32_t halo_box[3] = {(cuuint32_t)cols, (cuuint32_t)rows, 1};
-  const cuuint32_t prev_box[3] = {(cuuint32_t)(f64 ? zm_pcols<double>() : zm_pcols<float>()),
-                                  (cuuint32_t)(f64 ? zm_ty<double>() : zm_ty<float>()), 1};
+  const cuuint32_t prev_box[3] = {(cuuint32_t)(f64 ? zm_pcols<double>() : zm_pcols<float>()), (cuuint32_t)pty, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   for (int s = 0; s < 2; ++s)
     for (int q = 0; q < NF; ++q) {
@@ -527,12 +527,13 @@ mhd_status halo_end(mhd_mesh* m) {
 // along unsplit axes the whole extent is inner (its halo is a self copy).  `thick` is the slab
 // width per axis: the radius r = 3 for the NCCL schedule, wider for the peer-memory schedule so
 // that the slabs run on the tiled kernel (a superset of the cells within r of a split boundary).
-void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer, const int thick_in[3]) {
+void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer, const int thick_in[3],
+                   bool all_axes = false) {
   const int n[3] = {m->g.nx, m->g.ny, m->g.nz};
   bool split[3];
   int thick[3];
   for (int a = 0; a < 3; ++a) {
-    split[a] = m->P[a] > 1;
+    split[a] = m->P[a] > 1 || all_axes;
     thick[a] = std::max(m->info.radius, std::min(thick_in[a], n[a] / 2));
     inner.lo[a] = split[a] ? thick[a] : 0;
     inner.ext[a] = split[a] ? n[a] - 2 * thick[a] : n[a];
@@ -584,7 +585,7 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   if (!m->halo_valid) p2p_halo_copy<T>(m);
   Region inner;
   std::vector<Region> outer;
-  const int thick[3] = {zm_tx<T>(), zm_ty<T>(), 8};
+  const int thick[3] = {zm_tx<T>(), 8, 8};
   split_regions(m, inner, outer, thick);
   const unsigned long long s = ++m->seq;
   {
@@ -604,16 +605,53 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   return MHD_OK;
 }
 
+// One rank: the periodic self-copy of the halo runs on the side stream, concurrently with
+// the update of the cells at least one tile away from every face (which read no halo); the
+// boundary slabs follow once the copy is done.
+template <typename T>
+mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
+  Region inner;
+  std::vector<Region> outer;
+  const int thick[3] = {zm_tx<T>(), 8, 8};
+  split_regions(m, inner, outer, thick, true);
+  if (inner.ext[0] <= 0 || !m->self_list.n) {  // too small to split: copy, then update everything
+    const Fields<T> F = m->fields<T>(m->cur);
+    if (m->self_list.n) {
+      PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
+      launch_segments<T>(m->stream, F, m->g, m->self_list, SEG_SELF, nullptr);
+      m->launches++;
+    }
+    const Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
+    update_region<T>(m, full, k, dt, rhs_out);
+    CU(cudaGetLastError());
+    return MHD_OK;
+  }
+  CU(cudaEventRecord(m->ev_ready, m->stream));
+  CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
+  {
+    PhaseTimer t(m, m->comm_stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
+    launch_segments<T>(m->comm_stream, m->fields<T>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
+    m->launches++;
+  }
+  CU(cudaEventRecord(m->ev_halo, m->comm_stream));
+  update_region<T>(m, inner, k, dt, rhs_out);
+  CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
+  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out);
+  CU(cudaGetLastError());
+  return MHD_OK;
+}
+
 template <typename T>
 mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   if (m->exchange == 1) return substep_p2p<T>(m, k, dt, rhs_out);
+  if (!m->distributed()) return substep_local<T>(m, k, dt, rhs_out);
   mhd_status st = halo_begin<T>(m);
   if (st != MHD_OK) return st;
   Region inner;
   std::vector<Region> outer;
   // slabs one tile thick so that they run on the tiled kernel; the exchange stays hidden behind
   // the (smaller) inner segment
-  const int thick[3] = {zm_tx<T>(), zm_ty<T>(), 8};
+  const int thick[3] = {zm_tx<T>(), 8, 8};
   split_regions(m, inner, outer, thick);
   update_region<T>(m, inner, k, dt, rhs_out);
   st = halo_end<T>(m);
@@ -798,7 +836,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->pack_list = make_list(*m, false, true);
   m->unpack_list = make_list(*m, false, false);
   cudaError_t e = cudaMemsetAsync(m->ws, 0, m->L.total, m->stream);
-  if (e == cudaSuccess && info->nranks > 1) {
+  if (e == cudaSuccess) {  // side stream: halo exchange (N > 1) or the periodic self-copy (N = 1)
     int lo, hi;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     e = cudaStreamCreateWithPriority(&m->comm_stream, cudaStreamNonBlocking, hi);

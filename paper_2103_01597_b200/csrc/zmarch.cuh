@@ -55,7 +55,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 
 template <typename T, int RAD>
 struct ZCfg {
-  static constexpr int TX = zm_tx<T>(), TY = zm_ty<T>();
+  static constexpr int TX = zm_tx<T>(), TY = zm_ty<T, RAD>();
   static constexpr int ES = (int)sizeof(T);
   static constexpr int COLS = zm_cols<T, RAD>();
   static constexpr int ROWS = zm_rows<T, RAD>();
