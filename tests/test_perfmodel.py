@@ -38,3 +38,36 @@ def test_b200_model_is_compute_bound():
     for g in (2, 4, 8):
         m = perfmodel.b200((512,) * 3, g, 12.3)
         assert m["tau_q"] < 0.25 * m["tau_w"] and abs(m["efficiency"] - 1.0) < 1e-12
+
+
+def test_eq5_brute_force_optimum():
+    """Eq. 5 by exhaustive search.  For cubic N the Morton partition P:557 is always among
+    the optima ("minimizes, or nearly minimizes"); remote halo counts as in SURVEY 8(e):
+    4 GPUs tie (4,1,1) = (2,2,1) at 1,609,944 remote cells of 512^3; at 8, (2,2,2) = 1,207,512
+    beats (4,2,1) = 1,212,120."""
+    n = (512,) * 3
+    for cp in (2, 4, 8, 16, 32, 64):
+        for selfwrap in (False, True):
+            q, arg = perfmodel.optimal_decompositions(n, cp, periodic_self=selfwrap)
+            assert perfmodel.morton_partition(cp) in arg
+            # brute force really is the minimum over every factorisation
+            allq = [perfmodel.halo_q(n, P, 3, selfwrap) for P in perfmodel.factorizations(cp)]
+            assert q == min(allq) and len(perfmodel.factorizations(cp)) == sum(
+                1 for a in range(1, cp + 1) for b in range(1, cp + 1) if cp % (a * b) == 0)
+    assert perfmodel.halo_q(n, (4, 1, 1)) // 2 == perfmodel.halo_q(n, (2, 2, 1)) // 2 == 1609944
+    assert perfmodel.halo_q(n, (4, 2, 1)) // 2 == 1212120
+    assert perfmodel.optimal_decompositions(n, 8, periodic_self=True) == (2 * 1207512, [(2, 2, 2)])
+    # non-cubic: the long axis is split first
+    q, arg = perfmodel.optimal_decompositions((1024, 512, 512), 2)
+    assert arg == [(2, 1, 1)]
+    # Q by hand for one case: (1024,512,512)/(2,1,1) = 512^3 blocks, all halo exchanged
+    assert q == 2 * (518 ** 3 - 512 ** 3)
+
+
+def test_row_wise_vs_morton_internode_faces():
+    """with 8 devices per node, C_P >> 8 and equal subdomains, a row-wise scan gives each
+    process 4 to 5 faces shared with inter-node neighbours; Z-order gives exactly 3."""
+    import collections
+    row = collections.Counter(perfmodel.internode_faces((16, 16, 16), 8, "row"))
+    mor = collections.Counter(perfmodel.internode_faces((16, 16, 16), 8, "morton"))
+    assert set(row) == {4, 5} and mor == {3: 4096}

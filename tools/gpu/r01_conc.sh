@@ -1,0 +1,12 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_conc_parity.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_conc_parity.log
+timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_conc_1.log 2>&1
+timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline --order 8 > gpurun_out/bench_conc_o8.log 2>&1
+timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline --scaling strong --grid 512 --steps 30 > gpurun_out/bench_conc_strong1.log 2>&1
+timeout 2400 python -m pytest tests/test_multigpu.py -q -k "not 8" > gpurun_out/pytest_conc_mgpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_conc_mgpu.log
+for ex in p2p nccl; do
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29651 bench.py --gpus 4 --e2e-steps 0 --exchange $ex > gpurun_out/bench_conc_weak4_$ex.log 2>&1
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29652 bench.py --gpus 4 --e2e-steps 0 --exchange $ex --scaling strong --grid 512 > gpurun_out/bench_conc_strong4_$ex.log 2>&1
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29654 bench.py --gpus 2 --e2e-steps 0 --exchange $ex > gpurun_out/bench_conc_weak2_$ex.log 2>&1
+done
+echo done
