@@ -333,12 +333,17 @@ def main():
             "cpu_baseline": cpu,
         }
         if dp_per_cell and up["ms"] > 0:
+            # FP64: the kernel is bound by on-chip work (FP64 pipe and shared-memory wavefronts,
+            # DESIGN.md 7), not by HBM, so the FP64 roof is the primary one and HBM secondary.
             upd_cells = up["bytes"] / (NF_BYTES[args.dtype] * (2 + 3 + 3) / 3)  # cells x substeps updated
             ach = dp_per_cell * upd_cells / (up["ms"] * 1e-3)
-            line["roofline_fp64"] = {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_LANE_OPS,
-                                     "unit": "DP lane-ops/s", "frac": ach / FP64_PEAK_LANE_OPS,
-                                     "dp_per_cell": dp_per_cell,
-                                     "peak_source": "measured DFMA microbenchmark (profiles/r01_fp64_lds_microbench.txt)"}
+            line["roofline_hbm"] = roofline
+            line["roofline"] = {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_LANE_OPS,
+                                "unit": "DP lane-ops/s", "frac": ach / FP64_PEAK_LANE_OPS,
+                                "traffic": traffic, "dp_per_cell": dp_per_cell,
+                                "kernel": roofline["kernel"], "avg_launch_ms": upd_ms,
+                                "peak_source": "measured DFMA microbenchmark, 17.09e12 lane-ops/s = 92 % of "
+                                               "148 SM x 64 FP64 lanes x 1.965 GHz (profiles/r01_fp64_lds_microbench.txt)"}
         print(json.dumps(line), flush=True)
     mesh.close()
     if dist is not None:

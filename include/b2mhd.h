@@ -207,15 +207,18 @@ mhd_status mhd_mesh_query(const mhd_mesh* mesh, int32_t P[3], int32_t coord[3],
 mhd_status mhd_launch_count(const mhd_mesh* mesh, int64_t* count);
 
 /* Per-phase device timing with CUDA events recorded on the stream each phase is
- * launched on (compute stream for updates and self copies; comm stream for pack,
- * exchange and unpack).  enable = 1 starts recording (and clears), 0 stops. */
+ * launched on (compute stream for the inner update and self copies; comm stream for
+ * pack, exchange, unpack and the outer slabs).  enable = 1 starts recording (and clears), 0 stops. */
 typedef enum {
-  MHD_PHASE_UPDATE = 0,   /* fused stencil + RHS + RK3 kernels (inner and outer) */
+  MHD_PHASE_UPDATE = 0,   /* fused stencil + RHS + RK3 kernel over the inner segment, or over
+                             the whole subdomain when it is not split */
   MHD_PHASE_SELF = 1,     /* periodic self-copy of the halo */
   MHD_PHASE_PACK = 2,     /* pack kernel */
   MHD_PHASE_EXCHANGE = 3, /* NCCL grouped send/recv */
   MHD_PHASE_UNPACK = 4,   /* unpack kernel */
-  MHD_NPHASES = 5
+  MHD_PHASE_OUTER = 5,    /* the same update kernels over the outer-shell slabs,
+                             launched on the comm stream after the halo arrives */
+  MHD_NPHASES = 6
 } mhd_phase;
 mhd_status mhd_profile_enable(mhd_mesh* mesh, int32_t enable);
 

@@ -246,7 +246,7 @@ def mhd_launch_count(mesh: int) -> int:
     return c.value
 
 
-PHASES = ("update", "self", "pack", "exchange", "unpack")
+PHASES = ("update", "self", "pack", "exchange", "unpack", "outer")
 
 
 def mhd_profile_enable(mesh: int, enable: bool) -> None:

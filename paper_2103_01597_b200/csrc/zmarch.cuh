@@ -53,6 +53,21 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Warp-group skew: the CTA's upper half of rows (the "leading" group) runs half an iteration
+// ahead of the lower half, so that one group's load-heavy derivative phase overlaps the other's
+// load-free RHS phase instead of both hitting the shared-memory pipe at once.  Two named barriers
+// (alternating by plane parity) replace the per-plane CTA barrier; the lagging group refills the
+// ring.
+#ifndef B2_ZM_SKEW
+#define B2_ZM_SKEW 1
+#endif
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
 template <typename T, int RAD>
 struct ZCfg {
   static constexpr int TX = zm_tx<T>(), TY = zm_ty<T, RAD>();
@@ -91,6 +106,11 @@ struct ZStep {
   int pcell;  // offset inside a field of the f_{k-1} tile
   int slot0;  // plane zb - r (first staged plane) has slot 0
   const RemoteMap<T>& rm;
+  bool lead;  // leading warp group (B2_ZM_SKEW): signals "past the loads of plane o" mid-iteration
+
+  __device__ __forceinline__ void signal_half(int o) const {
+    if (B2_ZM_SKEW && lead) bar_arrive(1 + (o & 1), Z::NT);
+  }
 
   __device__ __forceinline__ const T* slot_of(int plane) const {
     return ring + ((plane - slot0) % Z::NSLOT) * Z::SLOT + cell;
@@ -182,6 +202,7 @@ struct ZStep {
     }
 #pragma unroll
     for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % RAD] = at(s0, q, 0, 0);
+    signal_half(p);
   }
 
   // Derivatives of one vector field (u or A) at output plane o: first and second derivatives
@@ -237,6 +258,7 @@ struct ZStep {
     // velocity
     T u[3], gu[3][3], d2u[3][3], xu[3];
     vector_derivs<PH>(st, 0, sk, u, gu, d2u, xu);
+    signal_half(o);
     // log density and entropy
     T sc[2], gsc[2][3], lap[2];
 #pragma unroll
@@ -338,8 +360,9 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     mbar_wait(&mbar[rel % Z::NSLOT], (unsigned)((rel / Z::NSLOT) & 1));
   };
 
-  const ZStep<T, RAD, MODE, REMOTE> S{ring, prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
-                                      first, rm};
+  const bool lead = ty >= TY / 2;
+  const ZStep<T, RAD, MODE, REMOTE> S{ring,  prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
+                                      first, rm,    lead};
   March<T, RAD> st;
 #pragma unroll
   for (int v = 0; v < 2; ++v)
@@ -355,7 +378,13 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
 
   auto iter = [&](auto ph, int p) {
     constexpr int PH = decltype(ph)::value;
-    __syncthreads();  // every thread is done with iteration p - 1: its slot is refilled now
+    if (B2_ZM_SKEW) {
+      // lagging group: wait until the leading group is past the loads of plane p (and so done
+      // with plane p - 1), and every lagging thread is done with p - 1; then refill p - 1's slot
+      if (!lead) bar_sync(1 + (p & 1), Z::NT);
+    } else {
+      __syncthreads();  // every thread is done with iteration p - 1: its slot is refilled now
+    }
     if (tid == 0 && p + RAD + 1 <= ze + RAD - 1) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       issue(p + RAD + 1);
