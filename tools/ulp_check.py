@@ -54,8 +54,14 @@ def main():
         u, z = ulp_errors(ref[q], got[q])
         hist = {str(k): int(np.sum(np.round(u) == k)) for k in range(0, 4)}
         hist[">=4"] = int(np.sum(np.round(u) >= 4))
+        # the same error in ulps of the larger of the model value and the value before the step:
+        # where f + dt RHS cancels to near 0, Eq. 15's eps shrinks while the rounding of the
+        # increment does not
+        mm = np.maximum(np.abs(ref[q]), np.abs(st[q])).ravel()
+        u0 = np.abs(ref[q].ravel() - got[q].ravel()) / np.exp2(np.floor(np.log2(mm)) - 52)
         out["fields"][name] = {"max_ulps": float(u.max()), "mean_ulps": float(u.mean()), "hist": hist,
-                               "zeros_in_model": int(z.size)}
+                               "zeros_in_model": int(z.size), "frac_le_2ulps": float(np.mean(u <= 2.0)),
+                               "max_ulps_of_max_m_f0": float(u0.max())}
         worst = max(worst, float(u.max()))
     out["max_ulps"] = worst
     print(json.dumps(out))
