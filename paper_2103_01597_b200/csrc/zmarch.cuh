@@ -58,7 +58,8 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 // other's load-free RHS phase instead of both hitting the shared-memory pipe at once.  Two named
 // barriers (alternating by plane parity) replace the per-plane CTA barrier; the lagging group
 // refills the ring.  Measured (256^3, one B200): +15 % for the FP64 order-8 kernel (32x4 tile,
-// 4 warps per SM), -12 % FP64 / -17 % FP32 for order 6 (8 warps per SM), so only r = 4 uses it.
+// 4 warps per SM); slower with 8 warps per SM (-12 % FP64 / -17 % FP32 at order 6, -15 % FP32 at
+// order 8), so only the 4-row tiles use it.
 __device__ __forceinline__ void bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
@@ -85,7 +86,7 @@ struct ZCfg {
   static constexpr unsigned PREV_TX = (unsigned)(NF * TY * PCOLS * ES);
   static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128;
   static constexpr bool FITS = SMEM <= 227 * 1024;
-  static constexpr bool SKEW = RAD >= 4;
+  static constexpr bool SKEW = TY < 8;  // the 4-row tiles (FP64, r = 4)
 };
 
 // Register state carried along z by one thread.
