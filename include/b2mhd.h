@@ -153,9 +153,20 @@ mhd_status mhd_load(mhd_mesh* mesh, int32_t field, const void* src, int32_t src_
                     int32_t on_device);
 
 /* Copy the current state's local interior into dst.  Blocking when
- * on_device == 0 (synchronises the mesh stream). */
+ * on_device == 0 (synchronises the mesh stream); see mhd_store_async. */
 mhd_status mhd_store(mhd_mesh* mesh, int32_t field, void* dst, int32_t dst_dtype,
                      int32_t on_device);
+
+/* Asynchronous store into HOST memory, for snapshot pipelines: the interior of the
+ * current state's field is copied on the device (in stream order, after every
+ * update already enqueued) into an internal staging buffer owned by the mesh
+ * (allocated on first use: 8 * nx'*ny'*nz' * dst_dtype bytes), and the
+ * device->host transfer then runs on a separate copy stream, overlapping the
+ * calls that follow (the next mhd_load's host->device copy, the next updates).
+ * dst must stay valid and must not be read until mhd_synchronize returns; a
+ * second store_async of the same field first waits for the first one's transfer.
+ * Page-locked dst gives full-duplex overlap.  Errors as mhd_store. */
+mhd_status mhd_store_async(mhd_mesh* mesh, int32_t field, void* dst_host, int32_t dst_dtype);
 
 /* Test hook: copy the halo-inclusive local grid M' of one field of the current
  * state, (nz'+6) * (ny'+6) * (nx'+6) values in the mesh dtype, x fastest, to

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out
     }
     if (REMOTE) {
       remote_store<T, RAD>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, z, fn);
-      __threadfence_system();
+      if (rm.sys) __threadfence_system();
     }
   } else {
     const long long n = (long long)g.nx * g.ny * g.nz;

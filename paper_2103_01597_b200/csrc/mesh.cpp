@@ -16,9 +16,16 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
+
+// Wrap stores (periodic halo written by the update epilogue) vs a self-copy launch before every
+// update.  Measured (256^3 per GPU, profiles/r01/bench_wab*.json): wrap stores win with several
+// ranks (+17 % peer-memory at 4 GPUs, where the serial self-copy delayed every rank's sync; +-1 %
+// NCCL) and lose on one GPU (11.9 vs 12.4 Gcell/s: the epilogue costs more than the 0.09 ms copy),
+// so the default is "on iff nranks > 1".  B2MHD_WRAP=0/1 overrides it at mesh_create.
 
 #include "../../include/b2mhd.h"
 #include "kernels.h"
@@ -286,22 +293,44 @@ struct mhd_mesh {
   std::vector<void*> ipc_bases;     // opened IPC allocations (closed at destroy)
   unsigned long long seq = 0;       // operations that touched halos across ranks
   bool halo_valid = false;          // halos of the current state already delivered by the last update
+  bool self_valid = false;          // periodic self-wrap halo of the current state is up to date
+  // asynchronous stores (mhd_store_async): device staging, copy stream, per-field completion
+  char* stage = nullptr;
+  int stage_es = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_staged[NF] = {}, ev_d2h[NF] = {};
   SegList remote_list;              // remote segments with buf_off = peer slot (halo copy after a load)
   FlagSet peer_arrive, peer_done, my_arrive, my_done;
+  // The periodic self-wrap halo is written by the update kernels themselves: every cell
+  // within r of a face of an unsplit axis also stores its new value at its wrapped halo position
+  // (the same epilogue as the peer-memory send, with this rank's own state as the target), so the
+  // next substep needs no self-copy launch.  Slot `peers.size()` of the map is this rank.
+  bool wrap = false;
+  bool wrap_stores() const { return wrap && self_list.n > 0 && peers.size() < (size_t)kMaxPeers; }
   template <typename T>
-  RemoteMap<T> remote_map(int dest_state) const {
+  RemoteMap<T> remote_map(int dest_state, bool remote = true, bool self = false) const {
     RemoteMap<T> rm;
     memset(&rm, 0, sizeof(rm));
     for (int c = 0; c < 27; ++c) rm.peer_of[c] = -1;
-    for (size_t i = 0; i < peers.size() && i < (size_t)kMaxPeers; ++i)
+    rm.sys = remote && !peers.empty();
+    if (remote)
+      for (size_t i = 0; i < peers.size() && i < (size_t)kMaxPeers; ++i)
+        for (int q = 0; q < NF; ++q)
+          rm.f[i][q] = reinterpret_cast<T*>(peer_ws[peers[i].peer] + L.state_off[dest_state] +
+                                            (size_t)q * L.field_bytes) + L.origin;
+    const size_t me = peers.size();
+    if (self && wrap_stores())
       for (int q = 0; q < NF; ++q)
-        rm.f[i][q] = reinterpret_cast<T*>(peer_ws[peers[i].peer] + L.state_off[dest_state] + (size_t)q * L.field_bytes) +
-                     L.origin;
+        rm.f[me][q] = reinterpret_cast<T*>(ws + L.state_off[dest_state] + (size_t)q * L.field_bytes) + L.origin;
     for (auto& si : segs) {
-      if (si.self) continue;
       const int code = (si.s.offset[0] + 1) + 3 * (si.s.offset[1] + 1) + 9 * (si.s.offset[2] + 1);
-      for (size_t i = 0; i < peers.size(); ++i)
-        if (peers[i].peer == si.s.send_peer) rm.peer_of[code] = (signed char)i;
+      if (si.self) {
+        if (self && wrap_stores()) rm.peer_of[code] = (signed char)me;
+        continue;
+      }
+      if (remote)
+        for (size_t i = 0; i < peers.size(); ++i)
+          if (peers[i].peer == si.s.send_peer) rm.peer_of[code] = (signed char)i;
     }
     return rm;
   }
@@ -352,6 +381,20 @@ SegList make_list(const mhd_mesh& m, bool self, bool send) {
       d.src[a] = si.s.src_first[a];
       d.dst[a] = si.s.dst_first[a];
       d.ext[a] = si.s.extent[a];
+    }
+    if (self && d.ext[0] == m.info.radius && m.g.nx >= 32 / (int)m.info.dtype) {
+      // x-face self copies: widen the r-cell rows to one whole 32-byte sector (4 doubles, 8
+      // floats) so that every load and store is a full sector; the extra cells land in the
+      // unused row padding (left pad = 128 B, right pad checked) and are never read.
+      const int W = 32 / (int)m.info.dtype, extra = W - m.info.radius;
+      const bool fits = d.dst[0] < 0 || m.L.sy - m.L.xo - m.g.nx >= W;
+      if (extra > 0 && fits) {
+        if (d.dst[0] < 0) {
+          d.dst[0] -= extra;
+          d.src[0] -= extra;
+        }
+        d.ext[0] = W;
+      }
     }
     d.count = (long long)d.ext[0] * d.ext[1] * d.ext[2];
     d.buf_off = 0;
@@ -484,14 +527,21 @@ bool zmarch_ok(const mhd_mesh* m, const Region& r) {
   return false;
 }
 
+// Periodic self-copy of the halo, only when the last update did not already write it.
+template <typename T>
+void ensure_self(mhd_mesh* m) {
+  if (m->self_list.n && !m->self_valid) {
+    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
+    launch_segments<T>(m->stream, m->fields<T>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
+    m->launches++;
+  }
+  m->self_valid = true;
+}
+
 template <typename T>
 mhd_status halo_begin(mhd_mesh* m) {
   const Fields<T> F = m->fields<T>(m->cur);
-  if (m->self_list.n) {
-    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
-    launch_segments<T>(m->stream, F, m->g, m->self_list, SEG_SELF, nullptr);
-    m->launches++;
-  }
+  ensure_self<T>(m);
   if (!m->distributed() || m->peers.empty()) return MHD_OK;
   if (!m->comm) return fail(MHD_ENCCL, "mhd_comm_init was not called");
   CU(cudaEventRecord(m->ev_ready, m->stream));
@@ -578,12 +628,7 @@ void p2p_halo_copy(mhd_mesh* m) {
 
 template <typename T>
 mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
-  const Fields<T> F = m->fields<T>(m->cur);
-  if (m->self_list.n) {
-    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
-    launch_segments<T>(m->stream, F, m->g, m->self_list, SEG_SELF, nullptr);
-    m->launches++;
-  }
+  ensure_self<T>(m);
   if (!m->halo_valid) p2p_halo_copy<T>(m);
   Region inner;
   std::vector<Region> outer;
@@ -600,31 +645,33 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
     launch_p2p_sync(m->comm_stream, m->peer_arrive, m->my_arrive, m->my_done, s);
     m->launches++;
   }
-  const RemoteMap<T> rm = m->remote_map<T>(1 - m->cur);
+  const RemoteMap<T> rm = m->remote_map<T>(1 - m->cur, true, true);
   for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, rhs_out ? nullptr : &rm, m->comm_stream);
   launch_p2p_signal(m->comm_stream, m->peer_done, s);
   m->launches++;
   CU(cudaEventRecord(m->ev_halo, m->comm_stream));
-  update_region<T>(m, inner, k, dt, rhs_out);
+  const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
+  update_region<T>(m, inner, k, dt, rhs_out, rhs_out || !m->wrap_stores() ? nullptr : &wm);
   CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
-  if (!rhs_out) m->halo_valid = true;  // the neighbours are delivering the new state's halo
+  if (!rhs_out) {
+    m->halo_valid = true;  // the neighbours are delivering the new state's halo
+    m->self_valid = m->wrap_stores();
+  }
   CU(cudaGetLastError());
   return MHD_OK;
 }
 
-// One rank: the periodic self-copy of the halo, then one update launch over the whole
-// grid.  (Overlapping the copy with an inner segment and updating the boundary slabs on the side
-// stream was measured slower, 11.4 vs 12.4 Gcell/s at 256^3: the thin slab launches cost more
-// than the 0.1 ms copy they hide.)
+// One rank: one update launch over the whole grid; its epilogue also writes the periodic halo of
+// the new state (wrap stores), so the self-copy runs only after a load.  (Overlapping a self-copy
+// with an inner segment and updating the boundary slabs on the side stream was measured slower,
+// 11.4 vs 12.4 Gcell/s at 256^3.)
 template <typename T>
 mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
-  if (m->self_list.n) {
-    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
-    launch_segments<T>(m->stream, m->fields<T>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
-    m->launches++;
-  }
+  ensure_self<T>(m);
   const Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
-  update_region<T>(m, full, k, dt, rhs_out);
+  const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
+  update_region<T>(m, full, k, dt, rhs_out, rhs_out || !m->wrap_stores() ? nullptr : &wm);
+  if (!rhs_out) m->self_valid = m->wrap_stores();
   CU(cudaGetLastError());
   return MHD_OK;
 }
@@ -641,15 +688,18 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   // high-priority comm stream, concurrently with the inner segment on the compute stream
   const int thick[3] = {zm_tx<T>(), 8, 8};
   split_regions(m, inner, outer, thick);
+  const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
+  const RemoteMap<T>* w = rhs_out || !m->wrap_stores() ? nullptr : &wm;
   if (m->peers.empty()) {
-    update_region<T>(m, inner, k, dt, rhs_out);
-    for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out);
+    update_region<T>(m, inner, k, dt, rhs_out, w);
+    for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, w);
   } else {
-    for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, nullptr, m->comm_stream);
+    for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, w, m->comm_stream);
     CU(cudaEventRecord(m->ev_halo, m->comm_stream));
-    update_region<T>(m, inner, k, dt, rhs_out);
+    update_region<T>(m, inner, k, dt, rhs_out, w);
     CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
   }
+  if (!rhs_out) m->self_valid = m->wrap_stores();
   CU(cudaGetLastError());
   return MHD_OK;
 }
@@ -795,6 +845,8 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   if (!dev_workspace || !out) return fail(MHD_EINVAL, "null workspace or out");
   mhd_mesh* m = new mhd_mesh();
   m->info = *info;
+  m->wrap = info->nranks > 1;
+  if (const char* w = getenv("B2MHD_WRAP")) m->wrap = atoi(w) != 0;
   partition_xyz(info->nranks, m->P);
   coord_xyz(info->rank, m->coord);
   m->segs = build_segments(info, info->rank);
@@ -876,6 +928,15 @@ mhd_status mhd_mesh_destroy(mhd_mesh* m) {
   if (m->ev_ready) cudaEventDestroy(m->ev_ready);
   if (m->ev_halo) cudaEventDestroy(m->ev_halo);
   if (m->h_red) cudaFreeHost(m->h_red);
+  if (m->copy_stream) {
+    cudaStreamSynchronize(m->copy_stream);
+    cudaStreamDestroy(m->copy_stream);
+  }
+  for (int q = 0; q < NF; ++q) {
+    if (m->ev_staged[q]) cudaEventDestroy(m->ev_staged[q]);
+    if (m->ev_d2h[q]) cudaEventDestroy(m->ev_d2h[q]);
+  }
+  if (m->stage) cudaFree(m->stage);
   for (auto& v : m->recs)
     for (auto& r : v) {
       cudaEventDestroy(r.a);
@@ -892,6 +953,7 @@ mhd_status mhd_load(mhd_mesh* m, int32_t field, const void* src, int32_t src_dty
   if (src_dtype != MHD_F32 && src_dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "src dtype");
   m->next_k = 0;
   m->halo_valid = false;
+  m->self_valid = false;
   return m->info.dtype == MHD_F64 ? load_impl<double>(m, field, src, src_dtype, on_device)
                                   : load_impl<float>(m, field, src, src_dtype, on_device);
 }
@@ -901,6 +963,38 @@ mhd_status mhd_store(mhd_mesh* m, int32_t field, void* dst, int32_t dst_dtype, i
   if (dst_dtype != MHD_F32 && dst_dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "dst dtype");
   return m->info.dtype == MHD_F64 ? store_impl<double>(m, field, dst, dst_dtype, on_device)
                                   : store_impl<float>(m, field, dst, dst_dtype, on_device);
+}
+
+mhd_status mhd_store_async(mhd_mesh* m, int32_t field, void* dst, int32_t dst_dtype) {
+  if (!m || !dst || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad store argument");
+  if (dst_dtype != MHD_F32 && dst_dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "dst dtype");
+  const size_t bytes = (size_t)m->g.nx * m->g.ny * m->g.nz * (size_t)dst_dtype;
+  if (!m->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+    for (int q = 0; q < NF; ++q) {
+      CU(cudaEventCreateWithFlags(&m->ev_staged[q], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&m->ev_d2h[q], cudaEventDisableTiming));
+    }
+  }
+  if (m->stage_es != dst_dtype) {  // (re)allocate the staging for this dtype
+    CU(cudaStreamSynchronize(m->copy_stream));
+    CU(cudaStreamSynchronize(m->stream));
+    if (m->stage) CU(cudaFree(m->stage));
+    m->stage = nullptr;
+    CU(cudaMalloc(&m->stage, bytes * NF));
+    m->stage_es = dst_dtype;
+    for (int q = 0; q < NF; ++q) CU(cudaEventRecord(m->ev_d2h[q], m->copy_stream));
+  }
+  char* st = m->stage + bytes * (size_t)field;
+  CU(cudaStreamWaitEvent(m->stream, m->ev_d2h[field], 0));  // the previous transfer of this slot is done
+  mhd_status s = m->info.dtype == MHD_F64 ? store_impl<double>(m, field, st, dst_dtype, 1)
+                                          : store_impl<float>(m, field, st, dst_dtype, 1);
+  if (s != MHD_OK) return s;
+  CU(cudaEventRecord(m->ev_staged[field], m->stream));
+  CU(cudaStreamWaitEvent(m->copy_stream, m->ev_staged[field], 0));
+  CU(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyDeviceToHost, m->copy_stream));
+  CU(cudaEventRecord(m->ev_d2h[field], m->copy_stream));
+  return MHD_OK;
 }
 
 mhd_status mhd_store_grid(mhd_mesh* m, int32_t field, void* dst, int32_t on_device) {
@@ -921,14 +1015,14 @@ mhd_status mhd_halo_exchange(mhd_mesh* m) {
   if (!m) return fail(MHD_EINVAL, "null mesh");
   if (m->exchange == 1) {
     if (m->info.dtype == MHD_F64) {
-      launch_segments<double>(m->stream, m->fields<double>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
+      ensure_self<double>(m);
       p2p_halo_copy<double>(m);
     } else {
-      launch_segments<float>(m->stream, m->fields<float>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
+      ensure_self<float>(m);
       p2p_halo_copy<float>(m);
     }
     launch_p2p_wait(m->stream, m->my_done, m->seq);  // the neighbours' copies into this halo have landed
-    m->launches += 2;
+    m->launches += 1;
     CU(cudaGetLastError());
     return MHD_OK;
   }
@@ -1002,6 +1096,7 @@ mhd_status mhd_synchronize(mhd_mesh* m) {
   if (!m) return fail(MHD_EINVAL, "null mesh");
   CU(cudaStreamSynchronize(m->stream));
   if (m->comm_stream) CU(cudaStreamSynchronize(m->comm_stream));
+  if (m->copy_stream) CU(cudaStreamSynchronize(m->copy_stream));
   CU(cudaGetLastError());
   return MHD_OK;
 }
@@ -1107,6 +1202,7 @@ mhd_status mhd_p2p_open(mhd_mesh* m, const void* blobs) {
   m->remote_list.nblocks = nb;
   m->exchange = 1;
   m->halo_valid = false;
+  m->self_valid = false;
   return MHD_OK;
 }
 
@@ -1116,6 +1212,7 @@ mhd_status mhd_set_exchange(mhd_mesh* m, int32_t mode) {
   if (mode == 0 && m->info.nranks > 1 && !m->comm) return fail(MHD_ENCCL, "mhd_comm_init first");
   m->exchange = m->info.nranks > 1 ? mode : 0;
   m->halo_valid = false;
+  m->self_valid = false;
   return MHD_OK;
 }
 

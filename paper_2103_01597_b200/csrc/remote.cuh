@@ -19,7 +19,9 @@ constexpr int kMaxPeers = 7;  // distinct neighbours of a (2,2,2) Morton block
 template <typename T>
 struct RemoteMap {
   T* f[kMaxPeers][NF];       // origins of the destination state's fields in each peer's workspace
-  signed char peer_of[27];   // (ox+1) + 3 (oy+1) + 9 (oz+1)  ->  peer slot, -1: self copy or not exchanged
+  signed char peer_of[27];   // (ox+1) + 3 (oy+1) + 9 (oz+1)  ->  slot, -1: not stored by the update
+  int sys;                   // 1: some slot is another GPU (a system-scope fence ends the kernel);
+                             // 0: only this rank's own periodic halo (wrap stores)
 };
 
 // Store the 8 new values of cell (x, y, z) into every neighbour halo that holds a copy of it.

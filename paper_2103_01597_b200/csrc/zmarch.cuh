@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
   };
 #pragma unroll 1
   for (int p = first; p < ze; p += RAD) unroll_phases<RAD>(iter, p, ze);
-  if (REMOTE) __threadfence_system();  // peer halo stores visible before the completion signal
+  if (REMOTE && rm.sys) __threadfence_system();  // peer halo stores visible before the completion signal
 }
 
 constexpr int kNZC = 64;

@@ -87,6 +87,15 @@ class Mesh:
             torch.cuda.current_stream(self.device).wait_stream(self.stream)
         return out
 
+    def store_async(self, out):
+        """Enqueue the store of the current state into the host tensor `out` (8, nz', ny', nx'),
+        pinned for overlap; `out` is complete after synchronize()."""
+        assert not out.is_cuda
+        dt = self._dt_of(out)
+        for q in range(8):
+            native.mhd_store_async(self.handle, q, out[q].data_ptr(), dt)
+        return out
+
     def store_grid(self):
         """Halo-inclusive local grids, (8, nz'+2r, ny'+2r, nx'+2r), on the host (test hook)."""
         sh = tuple(v + 2 * self.radius for v in self.shape)

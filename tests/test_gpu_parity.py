@@ -52,6 +52,16 @@ def test_load_store_roundtrip_bitwise(dtype):
     pinned = torch.empty_like(torch.from_numpy(st)).pin_memory()
     m.store(out=pinned)
     assert np.array_equal(pinned.numpy(), st)
+    # asynchronous store (staging + copy stream), interleaved with updates and reloads
+    a = torch.empty_like(pinned).pin_memory()
+    b = torch.empty_like(pinned).pin_memory()
+    m.store_async(a)
+    m.step(1e-4)
+    ref = m.store().cpu().numpy()
+    m.store_async(b)
+    m.load(st)
+    m.synchronize()
+    assert np.array_equal(a.numpy(), st) and np.array_equal(b.numpy(), ref)
     m.close()
 
 
@@ -73,6 +83,40 @@ def test_halo_exchange_sentinel_bitwise(corners, n):
                 for xs in (slice(0, 3), slice(-3, None)):
                     mask[zs, ys, xs] = False
     assert np.array_equal(grid[:, mask], expect[:, mask])
+    m.close()
+
+
+@pytest.mark.parametrize("corners", [False, True])
+@pytest.mark.parametrize("n,r", [((40, 24, 19), 3), ((37, 23, 16), 1), ((36, 20, 18), 4)])
+def test_wrap_store_halo_bitwise(corners, n, r, monkeypatch):
+    """After substeps (no explicit exchange) the halo of the new state, written by the update
+    kernel's epilogue (wrap stores), is the periodic wrap of its interior, bitwise.  (One
+    rank uses the self-copy by default; B2MHD_WRAP=1 forces the wrap stores.)"""
+    monkeypatch.setenv("B2MHD_WRAP", "1")
+    m, _ = _mesh(n, exchange_corners=corners, radius=r)
+    st = synth.pcg64_state((n[2], n[1], n[0]))
+    m.load(st)
+    for k in range(3):
+        m.substep(k, 1e-3)
+        grid = m.store_grid().numpy()
+        expect = np.stack([oracle.periodic_fill(oracle.with_halo(grid[q][r:-r, r:-r, r:-r], r), r=r)
+                           for q in range(8)])
+        mask = np.ones(grid.shape[1:], bool)
+        if not corners:
+            for zs in (slice(0, r), slice(-r, None)):
+                for ys in (slice(0, r), slice(-r, None)):
+                    for xs in (slice(0, r), slice(-r, None)):
+                        mask[zs, ys, xs] = False
+        assert np.array_equal(grid[:, mask], expect[:, mask]), k
+    wrapped = m.store().cpu().numpy()
+    m.close()
+    # the same substeps with the self-copy instead: bit-identical state
+    monkeypatch.setenv("B2MHD_WRAP", "0")
+    m, _ = _mesh(n, exchange_corners=corners, radius=r)
+    m.load(st)
+    for k in range(3):
+        m.substep(k, 1e-3)
+    assert np.array_equal(m.store().cpu().numpy(), wrapped)
     m.close()
 
 
