@@ -49,8 +49,9 @@ def parse():
     ap.add_argument("--corners", action="store_true")
     ap.add_argument("--order", type=int, choices=(2, 4, 6, 8), default=6,
                     help="stencil order 2r (P:829-830); the paper's benchmarks use 6")
-    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="nccl",
-                    help="N > 1: fused peer-memory boundary stores (p2p) or NCCL send/recv of packed segments")
+    ap.add_argument("--exchange", choices=("auto", "p2p", "nccl"), default="auto",
+                    help="N > 1: fused peer-memory boundary stores (p2p) or NCCL send/recv of packed segments; "
+                         "auto = p2p at N = 2, 4 (measured faster: DESIGN.md 10), NCCL otherwise")
     return ap.parse_args()
 
 
@@ -114,15 +115,16 @@ NF_BYTES = {"f64": 64, "f32": 32}  # 8 fields x sizeof(T)
 
 
 def cpu_baseline(n_glob, ds, params, dt, seconds_hint=True):
-    """The oracle as it stands, on the host cores: one RK3 step (3 substeps) of a 256 x 256 x 32
-    periodic slab of the bench workload (same cells, same per-cell work; bounded sample)."""
+    """The oracle as it stands, on the host cores: one RK3 step (3 substeps) of a periodic slab of
+    the bench workload of about 8 M cells (256 x 256 x 128 at 256^3; same cells, same per-cell
+    work; a bounded sample of a few seconds on the host cores)."""
     import numpy as np
 
     import oracle
     import synth
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
-    nz = 32
+    nz = max(16, min(n_glob[2], (8 << 20) // (n_glob[0] * n_glob[1])))
     st = synth.splitmix_state((n_glob[2], n_glob[1], n_glob[0]), (0, 0, 0), (nz, n_glob[1], n_glob[0]))
     oracle.integrate(st[:, :8], ds, params, dt, 0, substeps=1)  # warm the thread pool
     t0 = time.perf_counter()
@@ -146,7 +148,7 @@ def run_reference(args, n_glob, rank):
     ds = synth.spacing(n_glob)
     cores = len(os.sched_getaffinity(0))
     oracle.set_threads(cores)
-    nz = 16
+    nz = max(8, min(n_glob[2], (2 << 20) // (n_glob[0] * n_glob[1])))  # ~2 M cells per sample
     st = synth.splitmix_state((n_glob[2], n_glob[1], n_glob[0]), (0, 0, 0), (nz, n_glob[1], n_glob[0]))
     oracle.integrate(st[:, :4], ds, synth.P0, synth.DT, 0, substeps=1)
     cur = st
@@ -210,8 +212,9 @@ def main():
     dtype = b2.MHD_F64 if args.dtype == "f64" else b2.MHD_F32
     es = 8 if dtype == b2.MHD_F64 else 4
     ds = synth.spacing(n_glob)
+    exchange = args.exchange if args.exchange != "auto" else ("p2p" if world in (2, 4) else "nccl")
     mesh = b2.Mesh(n_glob, ds, synth.P0, dtype, rank=rank, nranks=world, exchange_corners=args.corners,
-                   kernel=args.kernel, exchange=args.exchange, radius=args.order // 2)
+                   kernel=args.kernel, exchange=exchange, radius=args.order // 2)
     nz, ny, nx = mesh.shape
     lo = tuple(c * n for c, n in zip(reversed(mesh.coord), (nz, ny, nx)))
     npdt = np.float64 if dtype == b2.MHD_F64 else np.float32
@@ -255,6 +258,21 @@ def main():
     mesh.profile(False)
     cells = n_glob[0] * n_glob[1] * n_glob[2]
     value = cells * 3 * args.steps / (ms_total * 1e-3) / 1e9
+
+    # per-substep time by k (k = 0 moves 128 B/cell, k = 1, 2 192 B/cell), from a few
+    # extra steps after the timed region, events between the substeps on the mesh stream
+    nk = max(1, min(10, args.steps))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nk)]
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(nk):
+        evs[i][0].record(mesh.stream)
+        for k in range(3):
+            mesh.substep(k, dt)
+            evs[i][k + 1].record(mesh.stream)
+    torch.cuda.synchronize()
+    per_k = [max_over_ranks(sum(evs[i][k].elapsed_time(evs[i][k + 1]) for i in range(nk)) / nk) for k in range(3)]
+    per_k_gcells = [cells / (t * 1e-3) / 1e9 for t in per_k]
 
     # finiteness over the timed window: any NaN/Inf invalidates the run
     finite = True
@@ -324,6 +342,7 @@ def main():
                        "exchange_corners": bool(args.corners),
                        "exchange": mesh.exchange, "order": args.order},
             "ms_per_substep": substep_ms,
+            "per_k": {"ms": per_k, "gcells": per_k_gcells, "steps": nk},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "roofline": roofline,

@@ -43,3 +43,16 @@ def test_multigpu_other_orders(radius):
         pytest.skip("needs 2 GPUs")
     rc, out = _run(2, (40, 36, 32), 0, port=29560 + radius, exchange="p2p", radius=radius)
     assert rc == 0, out[-4000:]
+
+
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_multigpu_full_size_bit_identity(nproc):
+    """BASELINE's 512^3 strong-scaling grid in bench.py's launch configuration (auto exchange):
+    every rank's state after one RK3 step equals the same region of a 1-GPU 512^3 run, bitwise."""
+    if _ngpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    env = dict(os.environ, MGPU_N="512,512,512", MGPU_EXCHANGE="p2p" if nproc in (2, 4) else "nccl")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={29580 + nproc}", os.path.join(ROOT, "tools", "mgpu_full.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
+    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
