@@ -315,9 +315,9 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            mesh.load(host)               # H2D of the step's input state (pinned)
+            mesh.load_async(host)         # H2D of the step's input state (pinned), own copy stream
             mesh.step(dt)
-            mesh.store_async(out_host)    # D2H of the step's result; overlaps the next step's H2D
+            mesh.store_async(out_host)    # D2H of the step's result, own copy stream
         mesh.synchronize()                # every step's result is on the host
         torch.cuda.synchronize()
         el = max_over_ranks(time.perf_counter() - t0)

@@ -168,6 +168,14 @@ mhd_status mhd_store(mhd_mesh* mesh, int32_t field, void* dst, int32_t dst_dtype
  * Page-locked dst gives full-duplex overlap.  Errors as mhd_store. */
 mhd_status mhd_store_async(mhd_mesh* mesh, int32_t field, void* dst_host, int32_t dst_dtype);
 
+/* Asynchronous load from HOST memory, the mirror of mhd_store_async: the
+ * host->device copy runs on the load copy stream into a second staging buffer
+ * (allocated on first use), overlapping the updates and transfers enqueued
+ * before it; the scatter into the current state then runs on the mesh stream in
+ * order.  Resets the substep counter like mhd_load.  src must stay valid and
+ * unmodified until mhd_synchronize returns. */
+mhd_status mhd_load_async(mhd_mesh* mesh, int32_t field, const void* src_host, int32_t src_dtype);
+
 /* Test hook: copy the halo-inclusive local grid M' of one field of the current
  * state, (nz'+6) * (ny'+6) * (nx'+6) values in the mesh dtype, x fastest, to
  * dst.  Halo cells never written (corners when exchange_corners = 0) hold

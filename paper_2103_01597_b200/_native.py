@@ -22,7 +22,7 @@ STATUS = {0: "MHD_OK", 1: "MHD_EINVAL", 2: "MHD_EDECOMP", 3: "MHD_ESMALL", 4: "M
 
 # every symbol include/b2mhd.h declares
 SYMBOLS = ("mhd_decompose", "mhd_segment_table", "mhd_workspace_bytes", "mhd_mesh_create", "mhd_nccl_unique_id",
-           "mhd_comm_init", "mhd_p2p_export", "mhd_p2p_open", "mhd_set_exchange", "mhd_mesh_destroy", "mhd_load", "mhd_store", "mhd_store_async", "mhd_store_grid", "mhd_halo_exchange",
+           "mhd_comm_init", "mhd_p2p_export", "mhd_p2p_open", "mhd_set_exchange", "mhd_mesh_destroy", "mhd_load", "mhd_store", "mhd_store_async", "mhd_load_async", "mhd_store_grid", "mhd_halo_exchange",
            "mhd_integrate_substep", "mhd_integrate_step", "mhd_reduce", "mhd_debug_rhs", "mhd_synchronize",
            "mhd_set_kernel", "mhd_mesh_query", "mhd_launch_count", "mhd_profile_enable", "mhd_profile_read", "mhd_status_str", "mhd_last_error",
            "mhd_abi_version")
@@ -70,6 +70,7 @@ def _load():
         "mhd_load": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32],
         "mhd_store": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32],
         "mhd_store_async": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32],
+        "mhd_load_async": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32],
         "mhd_store_grid": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32],
         "mhd_halo_exchange": [ctypes.c_void_p],
         "mhd_integrate_substep": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_double],
@@ -194,6 +195,10 @@ def mhd_load(mesh: int, field: int, ptr: int, dtype: int, on_device: bool) -> No
 
 def mhd_store(mesh: int, field: int, ptr: int, dtype: int, on_device: bool) -> None:
     check(lib.mhd_store(ctypes.c_void_p(mesh), field, ctypes.c_void_p(ptr), dtype, int(on_device)), "mhd_store")
+
+
+def mhd_load_async(mesh: int, field: int, ptr: int, dtype: int) -> None:
+    check(lib.mhd_load_async(ctypes.c_void_p(mesh), field, ctypes.c_void_p(ptr), dtype), "mhd_load_async")
 
 
 def mhd_store_async(mesh: int, field: int, ptr: int, dtype: int) -> None:

@@ -294,11 +294,16 @@ struct mhd_mesh {
   unsigned long long seq = 0;       // operations that touched halos across ranks
   bool halo_valid = false;          // halos of the current state already delivered by the last update
   bool self_valid = false;          // periodic self-wrap halo of the current state is up to date
-  // asynchronous stores (mhd_store_async): device staging, copy stream, per-field completion
-  char* stage = nullptr;
-  int stage_es = 0;
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_staged[NF] = {}, ev_d2h[NF] = {};
+  // asynchronous host I/O (mhd_store_async / mhd_load_async): per direction a device staging
+  // buffer (8 interior fields), a copy stream and per-field events: ev_dev = the device side of
+  // the slot is done (gathered for a store, scattered into the state for a load), ev_host = the
+  // PCIe copy of the slot is done
+  struct AsyncLane {
+    char* stage = nullptr;
+    int es = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_dev[NF] = {}, ev_host[NF] = {};
+  } aio[2];  // [0] store (device -> host), [1] load (host -> device)
   SegList remote_list;              // remote segments with buf_off = peer slot (halo copy after a load)
   FlagSet peer_arrive, peer_done, my_arrive, my_done;
   // The periodic self-wrap halo is written by the update kernels themselves: every cell
@@ -928,15 +933,17 @@ mhd_status mhd_mesh_destroy(mhd_mesh* m) {
   if (m->ev_ready) cudaEventDestroy(m->ev_ready);
   if (m->ev_halo) cudaEventDestroy(m->ev_halo);
   if (m->h_red) cudaFreeHost(m->h_red);
-  if (m->copy_stream) {
-    cudaStreamSynchronize(m->copy_stream);
-    cudaStreamDestroy(m->copy_stream);
+  for (auto& a : m->aio) {
+    if (a.st) {
+      cudaStreamSynchronize(a.st);
+      cudaStreamDestroy(a.st);
+    }
+    for (int q = 0; q < NF; ++q) {
+      if (a.ev_dev[q]) cudaEventDestroy(a.ev_dev[q]);
+      if (a.ev_host[q]) cudaEventDestroy(a.ev_host[q]);
+    }
+    if (a.stage) cudaFree(a.stage);
   }
-  for (int q = 0; q < NF; ++q) {
-    if (m->ev_staged[q]) cudaEventDestroy(m->ev_staged[q]);
-    if (m->ev_d2h[q]) cudaEventDestroy(m->ev_d2h[q]);
-  }
-  if (m->stage) cudaFree(m->stage);
   for (auto& v : m->recs)
     for (auto& r : v) {
       cudaEventDestroy(r.a);
@@ -965,35 +972,68 @@ mhd_status mhd_store(mhd_mesh* m, int32_t field, void* dst, int32_t dst_dtype, i
                                   : store_impl<float>(m, field, dst, dst_dtype, on_device);
 }
 
+// Lazily creates the lane's stream and events and (re)allocates its staging for dtype `es`.
+static mhd_status lane_ready(mhd_mesh* m, mhd_mesh::AsyncLane& a, int es) {
+  if (!a.st) {
+    CU(cudaStreamCreateWithFlags(&a.st, cudaStreamNonBlocking));
+    for (int q = 0; q < NF; ++q) {
+      CU(cudaEventCreateWithFlags(&a.ev_dev[q], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&a.ev_host[q], cudaEventDisableTiming));
+    }
+  }
+  if (a.es != es) {
+    CU(cudaStreamSynchronize(a.st));
+    CU(cudaStreamSynchronize(m->stream));
+    if (a.stage) CU(cudaFree(a.stage));
+    a.stage = nullptr;
+    CU(cudaMalloc(&a.stage, (size_t)m->g.nx * m->g.ny * m->g.nz * (size_t)es * NF));
+    a.es = es;
+    for (int q = 0; q < NF; ++q) {
+      CU(cudaEventRecord(a.ev_dev[q], m->stream));
+      CU(cudaEventRecord(a.ev_host[q], a.st));
+    }
+  }
+  return MHD_OK;
+}
+
 mhd_status mhd_store_async(mhd_mesh* m, int32_t field, void* dst, int32_t dst_dtype) {
   if (!m || !dst || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad store argument");
   if (dst_dtype != MHD_F32 && dst_dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "dst dtype");
-  const size_t bytes = (size_t)m->g.nx * m->g.ny * m->g.nz * (size_t)dst_dtype;
-  if (!m->copy_stream) {
-    CU(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
-    for (int q = 0; q < NF; ++q) {
-      CU(cudaEventCreateWithFlags(&m->ev_staged[q], cudaEventDisableTiming));
-      CU(cudaEventCreateWithFlags(&m->ev_d2h[q], cudaEventDisableTiming));
-    }
-  }
-  if (m->stage_es != dst_dtype) {  // (re)allocate the staging for this dtype
-    CU(cudaStreamSynchronize(m->copy_stream));
-    CU(cudaStreamSynchronize(m->stream));
-    if (m->stage) CU(cudaFree(m->stage));
-    m->stage = nullptr;
-    CU(cudaMalloc(&m->stage, bytes * NF));
-    m->stage_es = dst_dtype;
-    for (int q = 0; q < NF; ++q) CU(cudaEventRecord(m->ev_d2h[q], m->copy_stream));
-  }
-  char* st = m->stage + bytes * (size_t)field;
-  CU(cudaStreamWaitEvent(m->stream, m->ev_d2h[field], 0));  // the previous transfer of this slot is done
-  mhd_status s = m->info.dtype == MHD_F64 ? store_impl<double>(m, field, st, dst_dtype, 1)
-                                          : store_impl<float>(m, field, st, dst_dtype, 1);
+  auto& a = m->aio[0];
+  mhd_status s = lane_ready(m, a, dst_dtype);
   if (s != MHD_OK) return s;
-  CU(cudaEventRecord(m->ev_staged[field], m->stream));
-  CU(cudaStreamWaitEvent(m->copy_stream, m->ev_staged[field], 0));
-  CU(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyDeviceToHost, m->copy_stream));
-  CU(cudaEventRecord(m->ev_d2h[field], m->copy_stream));
+  const size_t bytes = (size_t)m->g.nx * m->g.ny * m->g.nz * (size_t)dst_dtype;
+  char* st = a.stage + bytes * (size_t)field;
+  CU(cudaStreamWaitEvent(m->stream, a.ev_host[field], 0));  // the previous transfer of this slot is done
+  s = m->info.dtype == MHD_F64 ? store_impl<double>(m, field, st, dst_dtype, 1)
+                               : store_impl<float>(m, field, st, dst_dtype, 1);
+  if (s != MHD_OK) return s;
+  CU(cudaEventRecord(a.ev_dev[field], m->stream));
+  CU(cudaStreamWaitEvent(a.st, a.ev_dev[field], 0));
+  CU(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyDeviceToHost, a.st));
+  CU(cudaEventRecord(a.ev_host[field], a.st));
+  return MHD_OK;
+}
+
+mhd_status mhd_load_async(mhd_mesh* m, int32_t field, const void* src, int32_t src_dtype) {
+  if (!m || !src || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad load argument");
+  if (src_dtype != MHD_F32 && src_dtype != MHD_F64) return fail(MHD_EUNSUPPORTED, "src dtype");
+  auto& a = m->aio[1];
+  mhd_status s = lane_ready(m, a, src_dtype);
+  if (s != MHD_OK) return s;
+  const size_t bytes = (size_t)m->g.nx * m->g.ny * m->g.nz * (size_t)src_dtype;
+  char* st = a.stage + bytes * (size_t)field;
+  CU(cudaStreamWaitEvent(a.st, a.ev_dev[field], 0));  // the previous scatter out of this slot is done
+  CU(cudaMemcpyAsync(st, src, bytes, cudaMemcpyHostToDevice, a.st));
+  CU(cudaEventRecord(a.ev_host[field], a.st));
+  CU(cudaStreamWaitEvent(m->stream, a.ev_host[field], 0));
+  m->next_k = 0;
+  m->halo_valid = false;
+  m->self_valid = false;
+  s = m->info.dtype == MHD_F64 ? load_impl<double>(m, field, st, src_dtype, 1)
+                               : load_impl<float>(m, field, st, src_dtype, 1);
+  if (s != MHD_OK) return s;
+  CU(cudaEventRecord(a.ev_dev[field], m->stream));
   return MHD_OK;
 }
 
@@ -1096,7 +1136,8 @@ mhd_status mhd_synchronize(mhd_mesh* m) {
   if (!m) return fail(MHD_EINVAL, "null mesh");
   CU(cudaStreamSynchronize(m->stream));
   if (m->comm_stream) CU(cudaStreamSynchronize(m->comm_stream));
-  if (m->copy_stream) CU(cudaStreamSynchronize(m->copy_stream));
+  for (auto& a : m->aio)
+    if (a.st) CU(cudaStreamSynchronize(a.st));
   CU(cudaGetLastError());
   return MHD_OK;
 }

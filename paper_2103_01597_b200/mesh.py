@@ -87,6 +87,16 @@ class Mesh:
             torch.cuda.current_stream(self.device).wait_stream(self.stream)
         return out
 
+    def load_async(self, state):
+        """Enqueue the load of a host tensor (8, nz', ny', nx') (pinned for overlap); the caller
+        keeps it alive and unmodified until synchronize()."""
+        assert not state.is_cuda and state.is_contiguous()
+        assert tuple(state.shape) == (8,) + tuple(self.shape), (state.shape, self.shape)
+        dt = self._dt_of(state)
+        for q in range(8):
+            native.mhd_load_async(self.handle, q, state[q].data_ptr(), dt)
+        self._keep = state
+
     def store_async(self, out):
         """Enqueue the store of the current state into the host tensor `out` (8, nz', ny', nx'),
         pinned for overlap; `out` is complete after synchronize()."""

@@ -62,6 +62,15 @@ def test_load_store_roundtrip_bitwise(dtype):
     m.load(st)
     m.synchronize()
     assert np.array_equal(a.numpy(), st) and np.array_equal(b.numpy(), ref)
+    # asynchronous load: a pipelined load -> step -> store sequence equals the blocking one
+    src = torch.from_numpy(st).pin_memory()
+    m.load_async(src)
+    m.step(1e-4)
+    m.store_async(a)
+    m.load_async(src)
+    m.store_async(b)
+    m.synchronize()
+    assert np.array_equal(a.numpy(), ref) and np.array_equal(b.numpy(), st)
     m.close()
 
 
