@@ -15,9 +15,9 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _run(nproc, N, corners=0, steps=3, port=29511, exchange="p2p", radius=3):
+def _run(nproc, N, corners=0, steps=3, port=29511, exchange="p2p", radius=3, dtype="f64"):
     env = dict(os.environ, MGPU_N=",".join(map(str, N)), MGPU_CORNERS=str(corners), MGPU_STEPS=str(steps),
-               MGPU_EXCHANGE=exchange, MGPU_RADIUS=str(radius))
+               MGPU_EXCHANGE=exchange, MGPU_RADIUS=str(radius), MGPU_DTYPE=dtype)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tools", "mgpu_check.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
@@ -42,6 +42,17 @@ def test_multigpu_other_orders(radius):
     if _ngpus() < 2:
         pytest.skip("needs 2 GPUs")
     rc, out = _run(2, (40, 36, 32), 0, port=29560 + radius, exchange="p2p", radius=radius)
+    assert rc == 0, out[-4000:]
+
+
+@pytest.mark.parametrize("nproc,exchange", [(2, "p2p"), (4, "nccl"), (4, "p2p")])
+def test_multigpu_fp32(nproc, exchange):
+    """The FP32 variant: bitwise halo (FP32-exact sentinels), P-GPU = 1-GPU bit for bit, oracle
+    within 1e-4 (R#18)."""
+    if _ngpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    rc, out = _run(nproc, (40, 32, 32), 0, port=29570 + nproc * 2 + (exchange == "p2p"), exchange=exchange,
+                   dtype="f32")
     assert rc == 0, out[-4000:]
 
 

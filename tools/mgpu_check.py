@@ -3,7 +3,8 @@
   1. halo exchange of a sentinel field (global linear index) is bit-exact against the oracle's
      periodic wrap of the global grid, on every rank (P:705, P:557);
   2. after `steps` RK3 steps the gathered P-GPU state is bit-identical to a 1-GPU run of the
-     same global grid done by rank 0 on its own device, and matches the oracle (<= 1e-11).
+     same global grid done by rank 0 on its own device, and matches the oracle (<= 1e-11 FP64;
+     FP32 (MGPU_DTYPE=f32): <= 1e-4 against the oracle fed the FP32-rounded state, R#18).
 
 Prints one JSON line per rank; exit code 0 iff every check passed.
 """
@@ -36,11 +37,13 @@ def main():
     corners = bool(int(os.environ.get("MGPU_CORNERS", "0")))
     exchange = os.environ.get("MGPU_EXCHANGE", "p2p")
     radius = int(os.environ.get("MGPU_RADIUS", "3"))
+    f32 = os.environ.get("MGPU_DTYPE", "f64") == "f32"
+    mdt, npdt = (b2.MHD_F32, np.float32) if f32 else (b2.MHD_F64, np.float64)
     ds = synth.spacing(N)
     res = {"rank": rank, "world": world, "N": N}
     ok = True
 
-    mesh = b2.Mesh(N, ds, synth.P0, b2.MHD_F64, rank=rank, nranks=world, exchange_corners=corners,
+    mesh = b2.Mesh(N, ds, synth.P0, mdt, rank=rank, nranks=world, exchange_corners=corners,
                    exchange=exchange, radius=radius)
     res["exchange"] = exchange
     Pz = tuple(reversed(mesh.P))
@@ -55,6 +58,9 @@ def main():
     for rep in range(reps):
         glob = (np.arange(8)[:, None, None, None] * 1e7 + np.arange(Nz * Ny * Nx).reshape(Nz, Ny, Nx)[None]
                 + rep * 1e9).astype(np.float64)
+        if f32:  # sentinels exactly representable in FP32
+            glob = (np.arange(8)[:, None, None, None] * 1e5 + np.arange(Nz * Ny * Nx).reshape(Nz, Ny, Nx)[None]
+                    + rep * 1e6).astype(np.float32)
         mesh.load(np.ascontiguousarray(G.local_interior(glob, Pz, cz)))
         mesh.halo_exchange()
         grid = mesh.store_grid().numpy()
@@ -77,7 +83,7 @@ def main():
     ok &= res["halo_bitwise"]
 
     # 2. RK3 steps: P GPUs vs 1 GPU (bit-identical) vs oracle
-    st = synth.pcg64_state((Nz, Ny, Nx))
+    st = synth.pcg64_state((Nz, Ny, Nx), dtype=npdt)
     mesh.load(np.ascontiguousarray(G.local_interior(st, Pz, cz)))
     for _ in range(steps):
         mesh.step(synth.DT)
@@ -89,7 +95,7 @@ def main():
         for c, part in parts:
             n = part.shape[1:]
             full[:, c[0] * n[0]:(c[0] + 1) * n[0], c[1] * n[1]:(c[1] + 1) * n[1], c[2] * n[2]:(c[2] + 1) * n[2]] = part
-        single = b2.Mesh(N, ds, synth.P0, b2.MHD_F64, radius=radius)
+        single = b2.Mesh(N, ds, synth.P0, mdt, radius=radius)
         single.load(st)
         for _ in range(steps):
             single.step(synth.DT)
@@ -103,7 +109,7 @@ def main():
             e = max(float(np.max(np.abs(full[q] - ref[q]) / np.maximum(np.abs(ref[q]), 1e-3 * np.max(np.abs(ref[q])))))
                     for q in range(8))
             res["oracle_field_err"] = e
-            ok &= e <= 1e-11
+            ok &= e <= (1e-4 if f32 else 1e-11)
     res["ok"] = bool(ok)
     print(json.dumps(res), flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
