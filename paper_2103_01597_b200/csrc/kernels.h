@@ -22,6 +22,8 @@ struct Fields {
 struct Geom {
   int nx, ny, nz;
   long long sy, sz;
+  int zwrap;  // z-marching kernel: fetch planes outside [0, nz) from their periodic image
+              // instead of the z halo (one rank, z unsplit); 0: read the halo planes
 };
 
 // One copy region of the halo machinery: cells of extent ext starting at src

@@ -279,6 +279,7 @@ struct mhd_mesh {
   std::vector<SegInfo> segs;
   std::vector<PeerXfer> peers;
   SegList self_list, pack_list, unpack_list;
+  SegList self_list_xy;  // self segments without a z component (z halo fetched by TMA wrap)
   ncclComm_t comm = nullptr;
   int cur = 0;
   int next_k = 0;
@@ -311,6 +312,7 @@ struct mhd_mesh {
   // (the same epilogue as the peer-memory send, with this rank's own state as the target), so the
   // next substep needs no self-copy launch.  Slot `peers.size()` of the map is this rank.
   bool wrap = false;
+  int slab_env[3] = {0, 0, 0};
   bool wrap_stores() const { return wrap && self_list.n > 0 && peers.size() < (size_t)kMaxPeers; }
   template <typename T>
   RemoteMap<T> remote_map(int dest_state, bool remote = true, bool self = false) const {
@@ -375,12 +377,13 @@ struct mhd_mesh {
 
 namespace {
 
-SegList make_list(const mhd_mesh& m, bool self, bool send) {
+SegList make_list(const mhd_mesh& m, bool self, bool send, bool no_z = false) {
   SegList Ls;
   memset(&Ls, 0, sizeof(Ls));
   int nb = 0;
   for (auto& si : m.segs) {
     if (si.self != self) continue;
+    if (no_z && si.s.offset[2] != 0) continue;
     SegDesc& d = Ls.s[Ls.n++];
     for (int a = 0; a < 3; ++a) {
       d.src[a] = si.s.src_first[a];
@@ -616,6 +619,20 @@ void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer,
   if (inner.ext[0] <= 0 || inner.ext[1] <= 0 || inner.ext[2] <= 0) inner.ext[0] = inner.ext[1] = inner.ext[2] = 0;
 }
 
+// Boundary-slab widths (x, y, z): one tile wide in x and y so that the slabs run on the tiled
+// kernel; in z 8 planes for NCCL (the slabs wait for the exchange: keep them small) and 16 for
+// the peer-memory exchange (the slabs run first, beside the inner segment: fewer planes lost to
+// the 2r-plane prologue).  Measured at 256^3 per GPU (profiles/r01/bench_slab*.json): p2p 4 GPUs
+// 44.6 -> 45.9, 2 GPUs 22.7 -> 23.1 Gcell/s; NCCL best at 8.  B2MHD_SLAB="x,y,z" overrides.
+template <typename T>
+void slab_thickness(const mhd_mesh* m, int thick[3]) {
+  thick[0] = zm_tx<T>();
+  thick[1] = 8;
+  thick[2] = m->exchange == 1 ? 16 : 8;
+  if (m->slab_env[0] > 0)
+    for (int a = 0; a < 3; ++a) thick[a] = m->slab_env[a];
+}
+
 // Peer-memory exchange.  Per substep: wait until every neighbour finished its
 // previous cross-rank operation; update the outer shell, storing boundary results locally and into
 // the neighbours' halos; publish; then update the inner segment (which needs no remote halo) while
@@ -637,7 +654,8 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   if (!m->halo_valid) p2p_halo_copy<T>(m);
   Region inner;
   std::vector<Region> outer;
-  const int thick[3] = {zm_tx<T>(), 8, 8};
+  int thick[3];
+  slab_thickness<T>(m, thick);
   split_regions(m, inner, outer, thick);
   const unsigned long long s = ++m->seq;
   // high-priority side stream: sync, boundary slabs (update + store into the neighbours' halos,
@@ -672,10 +690,21 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
 // 11.4 vs 12.4 Gcell/s at 256^3.)
 template <typename T>
 mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
-  ensure_self<T>(m);
   const Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
+  // z unsplit and the z-marching kernel on the whole grid: planes beyond the z faces are fetched
+  // from their periodic image by the TMA coordinates, so only the x/y halo is copied
+  const bool zw = !m->self_valid && m->variant != 1 && m->tmaps_ok && zmarch_ok<T>(m, full);
+  if (!m->self_valid && m->self_list.n) {
+    const SegList& L = zw ? m->self_list_xy : m->self_list;
+    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(L, sizeof(T)));
+    launch_segments<T>(m->stream, m->fields<T>(m->cur), m->g, L, SEG_SELF, nullptr);
+    m->launches++;
+  }
+  m->self_valid = !zw;  // the z halo of the current state stays stale with the TMA wrap
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
+  m->g.zwrap = zw ? 1 : 0;
   update_region<T>(m, full, k, dt, rhs_out, rhs_out || !m->wrap_stores() ? nullptr : &wm);
+  m->g.zwrap = 0;
   if (!rhs_out) m->self_valid = m->wrap_stores();
   CU(cudaGetLastError());
   return MHD_OK;
@@ -691,7 +720,8 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   std::vector<Region> outer;
   // slabs one tile thick so that they run on the tiled kernel; they follow the unpack on the
   // high-priority comm stream, concurrently with the inner segment on the compute stream
-  const int thick[3] = {zm_tx<T>(), 8, 8};
+  int thick[3];
+  slab_thickness<T>(m, thick);
   split_regions(m, inner, outer, thick);
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
   const RemoteMap<T>* w = rhs_out || !m->wrap_stores() ? nullptr : &wm;
@@ -852,6 +882,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->info = *info;
   m->wrap = info->nranks > 1;
   if (const char* w = getenv("B2MHD_WRAP")) m->wrap = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
   partition_xyz(info->nranks, m->P);
   coord_xyz(info->rank, m->coord);
   m->segs = build_segments(info, info->rank);
@@ -865,6 +896,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->g.nz = (int)m->L.n[2];
   m->g.sy = m->L.sy;
   m->g.sz = m->L.sz;
+  m->g.zwrap = 0;
   m->ws = static_cast<char*>(dev_workspace);
   m->stream = static_cast<cudaStream_t>(cuda_stream);
   // peers in rank order, each with a contiguous slice of the send and recv buffers
@@ -883,6 +915,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
     r0 += rcount[p];
   }
   m->self_list = make_list(*m, true, false);
+  m->self_list_xy = make_list(*m, true, false, true);
   m->pack_list = make_list(*m, false, true);
   m->unpack_list = make_list(*m, false, false);
   cudaError_t e = cudaMemsetAsync(m->ws, 0, m->L.total, m->stream);

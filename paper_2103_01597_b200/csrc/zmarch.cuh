@@ -348,7 +348,8 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     mbar_expect_tx(&mbar[s], Z::HALO_TX + (pv ? Z::PREV_TX : 0u));
     T* dst = ring + s * Z::SLOT;
 #pragma unroll
-    for (int q = 0; q < NF; ++q) tma_load_3d(dst + q * Z::FSZ, &tm.halo[q], &mbar[s], xs + xo, y0, P + RAD);
+    const int pz = !g.zwrap ? P : (P < 0 ? P + g.nz : (P >= g.nz ? P - g.nz : P));
+    for (int q = 0; q < NF; ++q) tma_load_3d(dst + q * Z::FSZ, &tm.halo[q], &mbar[s], xs + xo, y0, pz + RAD);
     if (pv) {
       T* pd = prevbuf + (po & 1) * NF * Z::PSZ;
 #pragma unroll
