@@ -280,6 +280,13 @@ struct mhd_mesh {
   std::vector<PeerXfer> peers;
   SegList self_list, pack_list, unpack_list;
   SegList self_list_xy;  // self segments without a z component (z halo fetched by TMA wrap)
+  SegList self_list_y;   // ... and with a y component (x faces written by the update epilogue)
+  bool xwrap = false;    // one rank: x faces by wrap stores (B2MHD_XWRAP=1)
+  bool x_valid = false;  // the x-face halo of the current state was written by the last update
+  // the inner segment stores the periodic halo of unsplit axes itself (B2MHD_INNER_WRAP=0: give
+  // the unsplit axes boundary slabs instead, measured 25 % slower at 4 GPUs: the extra one-tile
+  // slab launches serialise on the side stream, profiles/r01/bench_iw*.json)
+  bool inner_wrap = true;
   ncclComm_t comm = nullptr;
   int cur = 0;
   int next_k = 0;
@@ -341,6 +348,21 @@ struct mhd_mesh {
     }
     return rm;
   }
+  // One rank, x faces only: the x-face halo (offsets (+-1, 0, 0)) of the new state is written by
+  // the update epilogue; the y faces and xy edges are copied (whole coalesced rows) and the z halo
+  // is fetched by the TMA plane wrap.
+  template <typename T>
+  RemoteMap<T> xwrap_map(int dest_state) const {
+    RemoteMap<T> rm;
+    memset(&rm, 0, sizeof(rm));
+    for (int c = 0; c < 27; ++c) rm.peer_of[c] = -1;
+    rm.sys = 0;
+    for (int q = 0; q < NF; ++q)
+      rm.f[0][q] = reinterpret_cast<T*>(ws + L.state_off[dest_state] + (size_t)q * L.field_bytes) + L.origin;
+    rm.peer_of[(-1 + 1) + 3 * 1 + 9 * 1] = 0;
+    rm.peer_of[(1 + 1) + 3 * 1 + 9 * 1] = 0;
+    return rm;
+  }
   // profiling: (start, stop) event pairs per phase, with the algorithmic bytes of the launch
   struct Rec {
     cudaEvent_t a, b;
@@ -377,13 +399,14 @@ struct mhd_mesh {
 
 namespace {
 
-SegList make_list(const mhd_mesh& m, bool self, bool send, bool no_z = false) {
+SegList make_list(const mhd_mesh& m, bool self, bool send, bool no_z = false, bool need_y = false) {
   SegList Ls;
   memset(&Ls, 0, sizeof(Ls));
   int nb = 0;
   for (auto& si : m.segs) {
     if (si.self != self) continue;
     if (no_z && si.s.offset[2] != 0) continue;
+    if (need_y && si.s.offset[1] == 0) continue;
     SegDesc& d = Ls.s[Ls.n++];
     for (int a = 0; a < 3; ++a) {
       d.src[a] = si.s.src_first[a];
@@ -588,12 +611,13 @@ mhd_status halo_end(mhd_mesh* m) {
 // along unsplit axes the whole extent is inner (its halo is a self copy).  `thick` is the slab
 // width per axis: the radius r = 3 for the NCCL schedule, wider for the peer-memory schedule so
 // that the slabs run on the tiled kernel (a superset of the cells within r of a split boundary).
-void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer, const int thick_in[3]) {
+void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer, const int thick_in[3],
+                   bool wrap_axes = false) {
   const int n[3] = {m->g.nx, m->g.ny, m->g.nz};
   bool split[3];
   int thick[3];
   for (int a = 0; a < 3; ++a) {
-    split[a] = m->P[a] > 1;
+    split[a] = m->P[a] > 1 || wrap_axes;
     thick[a] = std::max(m->info.radius, std::min(thick_in[a], n[a] / 2));
     inner.lo[a] = split[a] ? thick[a] : 0;
     inner.ext[a] = split[a] ? n[a] - 2 * thick[a] : n[a];
@@ -656,7 +680,10 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   std::vector<Region> outer;
   int thick[3];
   slab_thickness<T>(m, thick);
-  split_regions(m, inner, outer, thick);
+  // optionally (B2MHD_INNER_WRAP=0) the unsplit axes get boundary slabs too, so that the inner
+  // segment runs the plain kernel
+  const bool wsplit = m->wrap_stores() && !m->inner_wrap;
+  split_regions(m, inner, outer, thick, wsplit);
   const unsigned long long s = ++m->seq;
   // high-priority side stream: sync, boundary slabs (update + store into the neighbours' halos,
   // the fused send), publish; the inner segment needs no remote halo and runs concurrently on the
@@ -674,7 +701,7 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   m->launches++;
   CU(cudaEventRecord(m->ev_halo, m->comm_stream));
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
-  update_region<T>(m, inner, k, dt, rhs_out, rhs_out || !m->wrap_stores() ? nullptr : &wm);
+  update_region<T>(m, inner, k, dt, rhs_out, rhs_out || !m->wrap_stores() || wsplit ? nullptr : &wm);
   CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
   if (!rhs_out) {
     m->halo_valid = true;  // the neighbours are delivering the new state's halo
@@ -694,18 +721,25 @@ mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
   // z unsplit and the z-marching kernel on the whole grid: planes beyond the z faces are fetched
   // from their periodic image by the TMA coordinates, so only the x/y halo is copied
   const bool zw = !m->self_valid && m->variant != 1 && m->tmaps_ok && zmarch_ok<T>(m, full);
+  // x faces already written by the previous update's epilogue (xwrap): copy the y rows only
+  const bool xw = zw && m->xwrap && m->x_valid;
   if (!m->self_valid && m->self_list.n) {
-    const SegList& L = zw ? m->self_list_xy : m->self_list;
+    const SegList& L = xw ? m->self_list_y : (zw ? m->self_list_xy : m->self_list);
     PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(L, sizeof(T)));
     launch_segments<T>(m->stream, m->fields<T>(m->cur), m->g, L, SEG_SELF, nullptr);
     m->launches++;
   }
   m->self_valid = !zw;  // the z halo of the current state stays stale with the TMA wrap
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
+  const RemoteMap<T> xm = m->xwrap_map<T>(1 - m->cur);
+  const bool use_x = !rhs_out && !m->wrap_stores() && zw && m->xwrap;
   m->g.zwrap = zw ? 1 : 0;
-  update_region<T>(m, full, k, dt, rhs_out, rhs_out || !m->wrap_stores() ? nullptr : &wm);
+  update_region<T>(m, full, k, dt, rhs_out, rhs_out ? nullptr : (m->wrap_stores() ? &wm : (use_x ? &xm : nullptr)));
   m->g.zwrap = 0;
-  if (!rhs_out) m->self_valid = m->wrap_stores();
+  if (!rhs_out) {
+    m->self_valid = m->wrap_stores();
+    m->x_valid = use_x;
+  }
   CU(cudaGetLastError());
   return MHD_OK;
 }
@@ -722,16 +756,18 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   // high-priority comm stream, concurrently with the inner segment on the compute stream
   int thick[3];
   slab_thickness<T>(m, thick);
-  split_regions(m, inner, outer, thick);
+  const bool wsplit = m->wrap_stores() && !m->inner_wrap;  // as in substep_p2p
+  split_regions(m, inner, outer, thick, wsplit);
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
   const RemoteMap<T>* w = rhs_out || !m->wrap_stores() ? nullptr : &wm;
+  const RemoteMap<T>* wi = wsplit ? nullptr : w;
   if (m->peers.empty()) {
-    update_region<T>(m, inner, k, dt, rhs_out, w);
+    update_region<T>(m, inner, k, dt, rhs_out, wi);
     for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, w);
   } else {
     for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, w, m->comm_stream);
     CU(cudaEventRecord(m->ev_halo, m->comm_stream));
-    update_region<T>(m, inner, k, dt, rhs_out, w);
+    update_region<T>(m, inner, k, dt, rhs_out, wi);
     CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
   }
   if (!rhs_out) m->self_valid = m->wrap_stores();
@@ -882,6 +918,8 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->info = *info;
   m->wrap = info->nranks > 1;
   if (const char* w = getenv("B2MHD_WRAP")) m->wrap = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_XWRAP")) m->xwrap = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_INNER_WRAP")) m->inner_wrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
   partition_xyz(info->nranks, m->P);
   coord_xyz(info->rank, m->coord);
@@ -916,6 +954,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   }
   m->self_list = make_list(*m, true, false);
   m->self_list_xy = make_list(*m, true, false, true);
+  m->self_list_y = make_list(*m, true, false, true, true);
   m->pack_list = make_list(*m, false, true);
   m->unpack_list = make_list(*m, false, false);
   cudaError_t e = cudaMemsetAsync(m->ws, 0, m->L.total, m->stream);
@@ -994,6 +1033,7 @@ mhd_status mhd_load(mhd_mesh* m, int32_t field, const void* src, int32_t src_dty
   m->next_k = 0;
   m->halo_valid = false;
   m->self_valid = false;
+  m->x_valid = false;
   return m->info.dtype == MHD_F64 ? load_impl<double>(m, field, src, src_dtype, on_device)
                                   : load_impl<float>(m, field, src, src_dtype, on_device);
 }
@@ -1063,6 +1103,7 @@ mhd_status mhd_load_async(mhd_mesh* m, int32_t field, const void* src, int32_t s
   m->next_k = 0;
   m->halo_valid = false;
   m->self_valid = false;
+  m->x_valid = false;
   s = m->info.dtype == MHD_F64 ? load_impl<double>(m, field, st, src_dtype, 1)
                                : load_impl<float>(m, field, st, src_dtype, 1);
   if (s != MHD_OK) return s;
@@ -1277,6 +1318,7 @@ mhd_status mhd_p2p_open(mhd_mesh* m, const void* blobs) {
   m->exchange = 1;
   m->halo_valid = false;
   m->self_valid = false;
+  m->x_valid = false;
   return MHD_OK;
 }
 
@@ -1287,6 +1329,7 @@ mhd_status mhd_set_exchange(mhd_mesh* m, int32_t mode) {
   m->exchange = m->info.nranks > 1 ? mode : 0;
   m->halo_valid = false;
   m->self_valid = false;
+  m->x_valid = false;
   return MHD_OK;
 }
 

@@ -129,6 +129,23 @@ def test_wrap_store_halo_bitwise(corners, n, r, monkeypatch):
     m.close()
 
 
+@pytest.mark.parametrize("n,r", [((64, 24, 19), 3), ((48, 20, 18), 4)])
+def test_xface_wrap_store_bit_identical(n, r, monkeypatch):
+    """One rank with B2MHD_XWRAP=1 (x-face halo written by the update epilogue, y rows copied,
+    z planes wrapped by TMA): the same state as the default schedule, bit for bit."""
+    st = synth.pcg64_state((n[2], n[1], n[0]))
+    out = []
+    for xw in ("0", "1"):
+        monkeypatch.setenv("B2MHD_XWRAP", xw)
+        m, _ = _mesh(n, radius=r)
+        m.load(st)
+        for _ in range(2):
+            m.step(1e-3)
+        out.append(m.store().cpu().numpy())
+        m.close()
+    assert np.array_equal(out[0], out[1])
+
+
 # ---- RHS parity ------------------------------------------------------------------------------------
 @pytest.mark.parametrize("params", [synth.P0, PSTRONG], ids=["P0", "strong"])
 @pytest.mark.parametrize("n,box", [((32, 32, 32), None), ((40, 32, 24), (2 * math.pi, 4 * math.pi, 6 * math.pi)),
