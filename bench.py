@@ -110,7 +110,10 @@ def peaks():
 # FP64 issue peak measured on this pool's B200 with a DFMA microbenchmark
 # (tools/microbench/fp64_peak.cu, profiles/r01_fp64_lds_microbench.txt): 17.09 T DFMA-lane/s.
 FP64_PEAK_LANE_OPS = 17.09e12
-DP_PER_CELL = 634.2          # executed DP instructions per cell-substep (ncu, zmarch_kernel<double>, k = 2)
+# executed FP64 lane operations (DADD + DMUL + DFMA) per cell-substep of zmarch_kernel<double, r>
+# by stencil order 2r (ncu smsp__sass_thread_inst_executed_op_d*_pred_on.sum over a k = 2 launch
+# at 256^3 / 256^3 cells; profiles/r01/ncu_dp_counts.txt)
+DP_PER_CELL = {2: 368.25, 4: 501.0, 6: 634.25, 8: 768.0}
 NF_BYTES = {"f64": 64, "f32": 32}  # 8 fields x sizeof(T)
 
 
@@ -290,7 +293,7 @@ def main():
     local_cells = nx * ny * nz
     # FP64 lane operations per cell-substep executed by the update kernel (DFMA + DADD + DMUL,
     # ncu source counters of zmarch_kernel<double>, profiles/r01/ncu_zmarch_*.txt)
-    dp_per_cell = DP_PER_CELL if dtype == b2.MHD_F64 else None
+    dp_per_cell = DP_PER_CELL[args.order] if dtype == b2.MHD_F64 else None
     ncu = {}
     try:
         ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_latest.json")))
