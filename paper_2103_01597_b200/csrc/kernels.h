@@ -79,8 +79,11 @@ void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scra
 // for FP64 at radius 4, whose (r + 2)-plane ring of 32 x 8 tiles would not fit in shared memory.
 template <typename T>
 constexpr int zm_tx() { return 32; }
+#ifndef B2_ZM_TY_F32
+#define B2_ZM_TY_F32 8
+#endif
 template <typename T, int RAD = 3>
-constexpr int zm_ty() { return (sizeof(T) == 8 && RAD >= 4) ? 4 : 8; }
+constexpr int zm_ty() { return sizeof(T) == 8 ? (RAD >= 4 ? 4 : 8) : (RAD >= 4 ? 8 : B2_ZM_TY_F32); }
 template <typename T>
 constexpr int zm_ch() { return 16 / (int)sizeof(T); }
 template <typename T, int RAD>
