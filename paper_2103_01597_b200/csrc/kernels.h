@@ -79,11 +79,15 @@ void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scra
 // for FP64 at radius 4, whose (r + 2)-plane ring of 32 x 8 tiles would not fit in shared memory.
 template <typename T>
 constexpr int zm_tx() { return 32; }
+// Tile height of the z-marching kernel.  FP64: 8 rows (4 at r = 4, where 8 does not fit in
+// shared memory).  FP32 at r = 3: 16 rows (512 threads, 16 warps per SM at 122 registers),
+// measured 21.4 vs 18.6 Gcell/s; at r = 1, 2 the 16-row tile was 10 % slower and at r = 4 it does
+// not fit (profiles/r01/bench_f32ty*.json).
 #ifndef B2_ZM_TY_F32
-#define B2_ZM_TY_F32 8
+#define B2_ZM_TY_F32 16
 #endif
 template <typename T, int RAD = 3>
-constexpr int zm_ty() { return sizeof(T) == 8 ? (RAD >= 4 ? 4 : 8) : (RAD >= 4 ? 8 : B2_ZM_TY_F32); }
+constexpr int zm_ty() { return sizeof(T) == 8 ? (RAD >= 4 ? 4 : 8) : (RAD == 3 ? B2_ZM_TY_F32 : 8); }
 template <typename T>
 constexpr int zm_ch() { return 16 / (int)sizeof(T); }
 template <typename T, int RAD>
