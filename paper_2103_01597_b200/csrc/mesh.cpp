@@ -287,6 +287,13 @@ struct mhd_mesh {
   // the unsplit axes boundary slabs instead, measured 25 % slower at 4 GPUs: the extra one-tile
   // slab launches serialise on the side stream, profiles/r01/bench_iw*.json)
   bool inner_wrap = true;
+  // persistent z-march schedule (one CTA per SM slot, equal plane ranges; B2MHD_PERSIST=1, one
+  // rank only): measured 8 % slower than the chunked grid (11.70 vs 12.66 Gcell/s,
+  // profiles/r01/bench_pers*.json) although it removes the wave tail and most chunk prologues:
+  // CTAs that run together no longer work on neighbouring tiles at the same z, so the halo
+  // rows they share stop hitting in L2.  Off by default.
+  bool persist = false;
+  int persist_env = -1;
   ncclComm_t comm = nullptr;
   int cur = 0;
   int next_k = 0;
@@ -528,7 +535,7 @@ void update_region_r(mhd_mesh* m, cudaStream_t st, const Region& r, int k, doubl
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
   PhaseTimer t(m, st, st == m->stream ? MHD_PHASE_UPDATE : MHD_PHASE_OUTER, cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
   if (zm)
-    launch_zmarch<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, rm);
+    launch_zmarch<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, rm, m->persist);
   else
     launch_direct<T, RAD>(st, in, out, m->g, r, C, k, rhs_out, rm);
   m->launches++;
@@ -734,7 +741,9 @@ mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
   const RemoteMap<T> xm = m->xwrap_map<T>(1 - m->cur);
   const bool use_x = !rhs_out && !m->wrap_stores() && zw && m->xwrap;
   m->g.zwrap = zw ? 1 : 0;
+  m->persist = m->persist_env == 1;
   update_region<T>(m, full, k, dt, rhs_out, rhs_out ? nullptr : (m->wrap_stores() ? &wm : (use_x ? &xm : nullptr)));
+  m->persist = false;
   m->g.zwrap = 0;
   if (!rhs_out) {
     m->self_valid = m->wrap_stores();
@@ -920,6 +929,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   if (const char* w = getenv("B2MHD_WRAP")) m->wrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_XWRAP")) m->xwrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_INNER_WRAP")) m->inner_wrap = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_PERSIST")) m->persist_env = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
   partition_xyz(info->nranks, m->P);
   coord_xyz(info->rank, m->coord);

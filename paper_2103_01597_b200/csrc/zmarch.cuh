@@ -21,6 +21,8 @@
 //    register set small.  The march is unrolled by r so the register history rotates by
 //    renaming, not by moves.
 #pragma once
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace b2 {
@@ -309,7 +311,7 @@ __device__ __forceinline__ void unroll_phases(F&& f, int p, int ze) {
 template <typename T, int RAD, int MODE, bool REMOTE>
 __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C,
-                  int k, T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm) {
+                  int k, T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm, int persist) {
   using Z = ZCfg<T, RAD>;
   constexpr int TX = Z::TX, TY = Z::TY;
   // Dynamic shared memory starts at the (1024-B aligned) base of the CTA window (no static
@@ -322,15 +324,8 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
 
   const int tid = (int)threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
-  const int x0 = r.lo[0] + (int)blockIdx.x * TX, y0 = r.lo[1] + (int)blockIdx.y * TY;
-  const int zb = r.lo[2] + (int)blockIdx.z * nzc;
-  const int ze = min(zb + nzc, r.lo[2] + r.ext[2]);
-  const int x = x0 + tx, y = y0 + ty;
-  const bool active = x < r.lo[0] + r.ext[0] && y < r.lo[1] + r.ext[1];
   const bool need_prev = MODE == 0 && k > 0;
-  const int first = zb - RAD;
-  const int xs = (x0 - RAD) & ~(Z::CH - 1);  // 16-byte aligned box starts (interior origin is 128-B aligned)
-  const int pxs = x0 & ~(Z::CH - 1);
+  const bool lead = ty >= TY / 2;
 
   if (tid == 0) {
     if (smem_u32(smem_raw) & 127) __trap();  // TMA destinations need 128-B alignment
@@ -339,65 +334,101 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
   }
   __syncthreads();
 
-  // one TMA transaction per staged plane P: its halo tile, plus f_{k-1} of output plane P - r.
-  // Memory coordinates: the pitched field has a halo of r cells (element = interior + r in y, z).
-  auto issue = [&](int P) {
-    const int s = (P - first) % Z::NSLOT;
-    const int po = P - RAD;
-    const bool pv = need_prev && po >= zb && po < ze;
-    mbar_expect_tx(&mbar[s], Z::HALO_TX + (pv ? Z::PREV_TX : 0u));
-    T* dst = ring + s * Z::SLOT;
-#pragma unroll
-    const int pz = !g.zwrap ? P : (P < 0 ? P + g.nz : (P >= g.nz ? P - g.nz : P));
-    for (int q = 0; q < NF; ++q) tma_load_3d(dst + q * Z::FSZ, &tm.halo[q], &mbar[s], xs + xo, y0, pz + RAD);
-    if (pv) {
-      T* pd = prevbuf + (po & 1) * NF * Z::PSZ;
-#pragma unroll
-      for (int q = 0; q < NF; ++q) tma_load_3d(pd + q * Z::PSZ, &tm.prev[q], &mbar[s], pxs + xo, y0 + RAD, po + RAD);
-    }
-  };
-  auto wait_plane = [&](int P) {
-    const int rel = P - first;
-    mbar_wait(&mbar[rel % Z::NSLOT], (unsigned)((rel / Z::NSLOT) & 1));
-  };
+  // One segment: the tile column at (x0, y0), output planes [zb, ze).  `base` = planes this CTA
+  // staged before the segment: ring slot and mbarrier phase of plane P are those of the running
+  // count base + (P - first).
+  auto segment = [&](const int x0, const int y0, const int zb, const int ze, const unsigned base) {
+    const int x = x0 + tx, y = y0 + ty;
+    const bool active = x < r.lo[0] + r.ext[0] && y < r.lo[1] + r.ext[1];
+    const int first = zb - RAD;
+    const int xs = (x0 - RAD) & ~(Z::CH - 1);  // 16-byte aligned box starts (interior origin is 128-B aligned)
+    const int pxs = x0 & ~(Z::CH - 1);
 
-  const bool lead = ty >= TY / 2;
-  const ZStep<T, RAD, MODE, REMOTE> S{ring,  prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
-                                      first, rm,    lead};
-  March<T, RAD> st;
+    // one TMA transaction per staged plane P: its halo tile, plus f_{k-1} of output plane P - r.
+    // Memory coordinates: the pitched field has a halo of r cells (element = interior + r in y, z).
+    auto issue = [&](int P) {
+      const int s = (int)((base + (unsigned)(P - first)) % Z::NSLOT);
+      const int po = P - RAD;
+      const bool pv = need_prev && po >= zb && po < ze;
+      mbar_expect_tx(&mbar[s], Z::HALO_TX + (pv ? Z::PREV_TX : 0u));
+      T* dst = ring + s * Z::SLOT;
+      const int pz = !g.zwrap ? P : (P < 0 ? P + g.nz : (P >= g.nz ? P - g.nz : P));
 #pragma unroll
-  for (int v = 0; v < 2; ++v)
+      for (int q = 0; q < NF; ++q) tma_load_3d(dst + q * Z::FSZ, &tm.halo[q], &mbar[s], xs + xo, y0, pz + RAD);
+      if (pv) {
+        T* pd = prevbuf + (po & 1) * NF * Z::PSZ;
 #pragma unroll
-    for (int j = 0; j < RAD; ++j)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
+        for (int q = 0; q < NF; ++q) tma_load_3d(pd + q * Z::PSZ, &tm.prev[q], &mbar[s], pxs + xo, y0 + RAD, po + RAD);
+      }
+    };
+    auto wait_plane = [&](int P) {
+      const unsigned rel = base + (unsigned)(P - first);
+      mbar_wait(&mbar[rel % Z::NSLOT], (rel / Z::NSLOT) & 1u);
+    };
 
-  if (tid == 0)
-    for (int P = first; P <= zb && P <= ze + RAD - 1; ++P) issue(P);
+    const ZStep<T, RAD, MODE, REMOTE> S{ring, prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
+                                        first - (int)(base % Z::NSLOT), rm, lead};
+    March<T, RAD> st;
 #pragma unroll
-  for (int i = 0; i < RAD; ++i) wait_plane(first + i);
+    for (int v = 0; v < 2; ++v)
+#pragma unroll
+      for (int j = 0; j < RAD; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
 
-  auto iter = [&](auto ph, int p) {
-    constexpr int PH = decltype(ph)::value;
-    if constexpr (Z::SKEW) {
-      // lagging group: wait until the leading group is past the loads of plane p (and so done
-      // with plane p - 1), and every lagging thread is done with p - 1; then refill p - 1's slot
-      if (!lead) bar_sync(1 + (p & 1), Z::NT);
-    } else {
-      __syncthreads();  // every thread is done with iteration p - 1: its slot is refilled now
-    }
-    if (tid == 0 && p + RAD + 1 <= ze + RAD - 1) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(p + RAD + 1);
-    }
-    wait_plane(p + RAD);  // plane p+r and f_{k-1}(p) have landed
-    if (p < zb)
-      S.template push_only<PH>(st, p);
-    else
-      S.template full<PH>(st, p, out, g, k, active, x, y, rhs_out);
-  };
+    if (tid == 0)
+      for (int P = first; P <= zb && P <= ze + RAD - 1; ++P) issue(P);
+#pragma unroll
+    for (int i = 0; i < RAD; ++i) wait_plane(first + i);
+
+    auto iter = [&](auto ph, int p) {
+      constexpr int PH = decltype(ph)::value;
+      if constexpr (Z::SKEW) {
+        // lagging group: wait until the leading group is past the loads of plane p (and so done
+        // with plane p - 1), and every lagging thread is done with p - 1; then refill p - 1's slot
+        if (!lead) bar_sync(1 + (p & 1), Z::NT);
+      } else {
+        __syncthreads();  // every thread is done with iteration p - 1: its slot is refilled now
+      }
+      if (tid == 0 && p + RAD + 1 <= ze + RAD - 1) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(p + RAD + 1);
+      }
+      wait_plane(p + RAD);  // plane p+r and f_{k-1}(p) have landed
+      if (p < zb)
+        S.template push_only<PH>(st, p);
+      else
+        S.template full<PH>(st, p, out, g, k, active, x, y, rhs_out);
+    };
 #pragma unroll 1
-  for (int p = first; p < ze; p += RAD) unroll_phases<RAD>(iter, p, ze);
+    for (int p = first; p < ze; p += RAD) unroll_phases<RAD>(iter, p, ze);
+  };
+
+  // The CTA's work is a range [u, u1) of "column planes": the gx * gy tile columns laid end to
+  // end, ez planes each.  Chunked grid: one z chunk of one column per CTA.  Persistent schedule:
+  // gridDim.x equal ranges, each spanning a few column segments.
+  const int gx = (r.ext[0] + TX - 1) / TX, gy = (r.ext[1] + TY - 1) / TY, ez = r.ext[2];
+  long long u, u1;
+  if (!persist) {
+    const int zs = (int)blockIdx.z * nzc;
+    u = ((long long)blockIdx.y * gx + blockIdx.x) * ez + zs;
+    u1 = u + min(nzc, ez - zs);
+  } else {
+    const long long total = (long long)gx * gy * ez;
+    const long long len = (total + gridDim.x - 1) / gridDim.x;
+    u = (long long)blockIdx.x * len;
+    u1 = min(total, u + len);
+  }
+  unsigned base = 0;
+#pragma unroll 1
+  while (u < u1) {
+    const int col = (int)(u / ez), zs = (int)(u % ez);
+    const int zlen = (int)min((long long)(ez - zs), u1 - u);
+    segment(r.lo[0] + (col % gx) * TX, r.lo[1] + (col / gx) * TY, r.lo[2] + zs, r.lo[2] + zs + zlen, base);
+    base += (unsigned)(zlen + 2 * RAD);
+    u += zlen;
+    if (u < u1) __syncthreads();  // every thread is done with the ring before the next prologue
+  }
   if (REMOTE && rm.sys) __threadfence_system();  // peer halo stores visible before the completion signal
 }
 
@@ -405,17 +436,25 @@ constexpr int kNZC = 64;
 
 template <typename T, int RAD, int MODE, bool REMOTE>
 void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm) {
+                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm, bool persist) {
   using Z = ZCfg<T, RAD>;
-  static bool attr = false;
-  if (!attr) {
+  static int resident = 0;  // CTAs of this instantiation that fit on the GPU at once
+  if (!resident) {
     cudaFuncSetAttribute(zmarch_kernel<T, RAD, MODE, REMOTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Z::SMEM);
-    attr = true;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, zmarch_kernel<T, RAD, MODE, REMOTE>, Z::NT, Z::SMEM);
+    resident = std::max(1, sms * std::max(1, per));
   }
   const int nzc = r.ext[2] < kNZC ? r.ext[2] : kNZC;
   dim3 grd((r.ext[0] + Z::TX - 1) / Z::TX, (r.ext[1] + Z::TY - 1) / Z::TY, (r.ext[2] + nzc - 1) / nzc);
-  zmarch_kernel<T, RAD, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm);
+  // persistent schedule when the chunked grid would take more than one wave (and the warp-group
+  // skew, whose barrier ids follow the plane parity, is off)
+  const bool pers = persist && !Z::SKEW && (long long)grd.x * grd.y * grd.z > resident;
+  if (pers) grd = dim3(resident, 1, 1);
+  zmarch_kernel<T, RAD, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm, pers ? 1 : 0);
 }
 
 }  // namespace zm
@@ -428,21 +467,21 @@ bool zmarch_supported(const Geom& g, const Region& r) {
 
 template <typename T, int RAD>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm) {
+                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm, bool persist) {
   if constexpr (zm::ZCfg<T, RAD>::FITS) {
     RemoteMap<T> none;
     if (rhs_out)
-      zm::launch_cfg<T, RAD, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none);
+      zm::launch_cfg<T, RAD, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none, persist);
     else if (rm)
-      zm::launch_cfg<T, RAD, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm);
+      zm::launch_cfg<T, RAD, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm, persist);
     else
-      zm::launch_cfg<T, RAD, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none);
+      zm::launch_cfg<T, RAD, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none, persist);
   }
 }
 
 #define B2_ZMARCH_INSTANTIATE(T, RAD)                                                                      \
   template bool zmarch_supported<T, RAD>(const Geom&, const Region&);                                       \
   template void launch_zmarch<T, RAD>(cudaStream_t, const TmapSet&, const Fields<T>&, const Geom&, const Region&, \
-                                      const Coef<T>&, int, T*, int, const RemoteMap<T>*);
+                                      const Coef<T>&, int, T*, int, const RemoteMap<T>*, bool);
 
 }  // namespace b2

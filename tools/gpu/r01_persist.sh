@@ -1,0 +1,14 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_persist.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_persist.log
+for i in 1 2; do
+timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_pers1_f64_$i.log 2>&1
+B2MHD_PERSIST=0 timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_pers0_f64_$i.log 2>&1
+done
+for o in 2 4 8; do
+timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline --order $o > gpurun_out/bench_pers1_o$o.log 2>&1
+B2MHD_PERSIST=0 timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline --order $o > gpurun_out/bench_pers0_o$o.log 2>&1
+done
+timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline --dtype f32 > gpurun_out/bench_pers1_f32.log 2>&1
+B2MHD_PERSIST=0 timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline --dtype f32 > gpurun_out/bench_pers0_f32.log 2>&1
+timeout 300 python bench.py --e2e-steps 0 --no-cpu-baseline --grid 512 --scaling strong --steps 30 > gpurun_out/bench_pers1_512.log 2>&1
+echo done
