@@ -24,6 +24,7 @@ struct Geom {
   long long sy, sz;
   int zwrap;  // z-marching kernel: fetch planes outside [0, nz) from their periodic image
               // instead of the z halo (one rank, z unsplit); 0: read the halo planes
+  int xwrap;  // z-marching kernel, plain variant: also store the periodic x faces of the output
 };
 
 // One copy region of the halo machinery: cells of extent ext starting at src

@@ -281,8 +281,18 @@ struct mhd_mesh {
   SegList self_list, pack_list, unpack_list;
   SegList self_list_xy;  // self segments without a z component (z halo fetched by TMA wrap)
   SegList self_list_y;   // ... and with a y component (x faces written by the update epilogue)
-  bool xwrap = false;    // one rank: x faces by wrap stores (B2MHD_XWRAP=1)
-  bool x_valid = false;  // the x-face halo of the current state was written by the last update
+  // Periodic x faces written by the plain z-march kernel's epilogue (Geom::xwrap: predicated
+  // stores of the cells within one sector of an x face; B2MHD_XWRAP=0 disables).  One rank:
+  // the y rows are then copied (0.014 ms instead of 0.06 ms for x and y) and the z planes are
+  // wrapped by TMA: 12.87 -> 13.1 Gcell/s FP64, 21.0 -> 22.2 FP32 (profiles/r01/bench_xw2_*).
+  // Several ranks with only x unsplit (4 GPUs): the inner segment uses it instead of the storing
+  // (REMOTE) variant.
+  bool xwrap = true;
+  bool x_valid = false;  // the x faces of the current state were written by the last update
+  bool x_fits() const {
+    const int64_t W = 32 / (int64_t)info.dtype;
+    return xwrap && L.sy - L.xo - g.nx >= W && g.nx >= 2 * W;
+  }
   // the inner segment stores the periodic halo of unsplit axes itself (B2MHD_INNER_WRAP=0: give
   // the unsplit axes boundary slabs instead, measured 25 % slower at 4 GPUs: the extra one-tile
   // slab launches serialise on the side stream, profiles/r01/bench_iw*.json)
@@ -353,21 +363,6 @@ struct mhd_mesh {
         for (size_t i = 0; i < peers.size(); ++i)
           if (peers[i].peer == si.s.send_peer) rm.peer_of[code] = (signed char)i;
     }
-    return rm;
-  }
-  // One rank, x faces only: the x-face halo (offsets (+-1, 0, 0)) of the new state is written by
-  // the update epilogue; the y faces and xy edges are copied (whole coalesced rows) and the z halo
-  // is fetched by the TMA plane wrap.
-  template <typename T>
-  RemoteMap<T> xwrap_map(int dest_state) const {
-    RemoteMap<T> rm;
-    memset(&rm, 0, sizeof(rm));
-    for (int c = 0; c < 27; ++c) rm.peer_of[c] = -1;
-    rm.sys = 0;
-    for (int q = 0; q < NF; ++q)
-      rm.f[0][q] = reinterpret_cast<T*>(ws + L.state_off[dest_state] + (size_t)q * L.field_bytes) + L.origin;
-    rm.peer_of[(-1 + 1) + 3 * 1 + 9 * 1] = 0;
-    rm.peer_of[(1 + 1) + 3 * 1 + 9 * 1] = 0;
     return rm;
   }
   // profiling: (start, stop) event pairs per phase, with the algorithmic bytes of the launch
@@ -707,8 +702,13 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   launch_p2p_signal(m->comm_stream, m->peer_done, s);
   m->launches++;
   CU(cudaEventRecord(m->ev_halo, m->comm_stream));
+  // inner segment: the periodic halo of the unsplit axes through the storing variant, the same
+  // kernel binary as the concurrent boundary slabs (the plain kernel with its x-face stores,
+  // the 1-GPU choice, ran 12 % slower here: two different z-march binaries side by side,
+  // profiles/r01/bench_x2_weak4_*.json)
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
-  update_region<T>(m, inner, k, dt, rhs_out, rhs_out || !m->wrap_stores() || wsplit ? nullptr : &wm);
+  const bool inner_wrap = !rhs_out && m->wrap_stores() && !wsplit;
+  update_region<T>(m, inner, k, dt, rhs_out, inner_wrap ? &wm : nullptr);
   CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
   if (!rhs_out) {
     m->halo_valid = true;  // the neighbours are delivering the new state's halo
@@ -726,10 +726,11 @@ template <typename T>
 mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
   const Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
   // z unsplit and the z-marching kernel on the whole grid: planes beyond the z faces are fetched
-  // from their periodic image by the TMA coordinates, so only the x/y halo is copied
-  const bool zw = !m->self_valid && m->variant != 1 && m->tmaps_ok && zmarch_ok<T>(m, full);
-  // x faces already written by the previous update's epilogue (xwrap): copy the y rows only
-  const bool xw = zw && m->xwrap && m->x_valid;
+  // from their periodic image by the TMA coordinates (the z halo is never materialised); the x
+  // faces are written by the previous update's epilogue, so only the y rows are copied
+  const bool zm = m->variant != 1 && m->tmaps_ok && zmarch_ok<T>(m, full);
+  const bool zw = !m->self_valid && zm;
+  const bool xw = zw && m->x_valid;
   if (!m->self_valid && m->self_list.n) {
     const SegList& L = xw ? m->self_list_y : (zw ? m->self_list_xy : m->self_list);
     PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(L, sizeof(T)));
@@ -738,13 +739,14 @@ mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
   }
   m->self_valid = !zw;  // the z halo of the current state stays stale with the TMA wrap
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
-  const RemoteMap<T> xm = m->xwrap_map<T>(1 - m->cur);
-  const bool use_x = !rhs_out && !m->wrap_stores() && zw && m->xwrap;
+  const bool use_x = !rhs_out && !m->wrap_stores() && zw && m->x_fits();
   m->g.zwrap = zw ? 1 : 0;
+  m->g.xwrap = use_x ? 1 : 0;
   m->persist = m->persist_env == 1;
-  update_region<T>(m, full, k, dt, rhs_out, rhs_out ? nullptr : (m->wrap_stores() ? &wm : (use_x ? &xm : nullptr)));
+  update_region<T>(m, full, k, dt, rhs_out, rhs_out || !m->wrap_stores() ? nullptr : &wm);
   m->persist = false;
   m->g.zwrap = 0;
+  m->g.xwrap = 0;
   if (!rhs_out) {
     m->self_valid = m->wrap_stores();
     m->x_valid = use_x;
@@ -769,7 +771,7 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   split_regions(m, inner, outer, thick, wsplit);
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
   const RemoteMap<T>* w = rhs_out || !m->wrap_stores() ? nullptr : &wm;
-  const RemoteMap<T>* wi = wsplit ? nullptr : w;
+  const RemoteMap<T>* wi = wsplit ? nullptr : w;  // same binary as the slabs (see substep_p2p)
   if (m->peers.empty()) {
     update_region<T>(m, inner, k, dt, rhs_out, wi);
     for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, w);
@@ -945,6 +947,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->g.sy = m->L.sy;
   m->g.sz = m->L.sz;
   m->g.zwrap = 0;
+  m->g.xwrap = 0;
   m->ws = static_cast<char*>(dev_workspace);
   m->stream = static_cast<cudaStream_t>(cuda_stream);
   // peers in rank order, each with a contiguous slice of the send and recv buffers

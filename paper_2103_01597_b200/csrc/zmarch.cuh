@@ -288,6 +288,18 @@ struct ZStep {
           out.f[q][gidx] = fn[q];
         }
         if (REMOTE) remote_store<T, RAD>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, o, fn);
+        if (!REMOTE && g.xwrap) {
+          // periodic x faces of this rank's own halo (x unsplit) written here: the cells in
+          // the first / last 32-byte sector of a row also go to the row padding on the other side
+          // (whole sectors: the extra cell lands in unused padding).  (Adding the y faces here
+          // pushed the kernel to 255 registers with spills: the y rows are copied instead.)
+          constexpr int W = 32 / (int)sizeof(T);
+          const long long sh = x < W ? (long long)g.nx : (x >= g.nx - W ? -(long long)g.nx : 0);
+          if (sh != 0) {
+#pragma unroll
+            for (int q = 0; q < NF; ++q) out.f[q][gidx + sh] = fn[q];
+          }
+        }
       } else {
         const long long n = (long long)g.nx * g.ny * g.nz;
         const long long li = ((long long)o * g.ny + y) * g.nx + x;

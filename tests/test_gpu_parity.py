@@ -131,8 +131,9 @@ def test_wrap_store_halo_bitwise(corners, n, r, monkeypatch):
 
 @pytest.mark.parametrize("n,r", [((64, 24, 19), 3), ((48, 20, 18), 4)])
 def test_xface_wrap_store_bit_identical(n, r, monkeypatch):
-    """One rank with B2MHD_XWRAP=1 (x-face halo written by the update epilogue, y rows copied,
-    z planes wrapped by TMA): the same state as the default schedule, bit for bit."""
+    """One rank: the x/y halo written by the plain kernel's predicated epilogue stores and the z
+    planes wrapped by TMA (the default, B2MHD_XWRAP=1) give the same state, bit for bit, as the
+    self-copy schedule (B2MHD_XWRAP=0)."""
     st = synth.pcg64_state((n[2], n[1], n[0]))
     out = []
     for xw in ("0", "1"):
