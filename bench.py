@@ -5,9 +5,11 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
 A bench "step" is one full RK3 step = 3 ISL iterations, each one pass of the whole
-hot path: self halo copy, pack -> NCCL exchange -> unpack (N > 1) overlapped with the inner
-update, outer update.  Metric (BASELINE.json): Gcell-updates/s per RK3 substep
-= global interior cells x substeps / time.
+hot path: the halo exchange (one GPU: periodic y rows copied, x faces written by
+the previous update's epilogue, z planes wrapped by TMA; N > 1: fused peer-memory stores by
+the boundary-slab kernels at N = 2, 4, or NCCL pack -> send/recv -> unpack) overlapped with the
+inner update, and the boundary-slab update.  Metric (BASELINE.json): Gcell-updates/s per RK3
+substep = global interior cells x substeps / time.
 
 Default workload: 256^3 FP64 per GPU (BASELINE configs[1] at N = 1; configs[3] weak scaling
 for N > 1: global grid = 256^3 x Morton partition, 512^3 at N = 8).  --scaling strong
