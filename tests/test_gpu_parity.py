@@ -147,6 +147,51 @@ def test_xface_wrap_store_bit_identical(n, r, monkeypatch):
     assert np.array_equal(out[0], out[1])
 
 
+@pytest.mark.parametrize("xwrap", ["0", "1"])
+def test_debug_rhs_after_steps(xwrap, monkeypatch):
+    """The RHS of a state reached by substeps (whose halo comes from the schedule's own
+    machinery: x faces from the previous epilogue, y rows copied, z planes wrapped by TMA) equals
+    the oracle's RHS of the stored interior; then stepping on gives the same state as a fresh
+    load of that interior."""
+    monkeypatch.setenv("B2MHD_XWRAP", xwrap)
+    n = (64, 24, 19)
+    m, ds = _mesh(n, params=PSTRONG)
+    st = synth.pcg64_state((n[2], n[1], n[0]))
+    m.load(st)
+    m.step(1e-4)
+    m.step(1e-4)
+    cur = m.store().cpu().numpy()
+    got = m.debug_rhs().cpu().numpy()
+    ref = oracle.rhs(cur, ds, PSTRONG)
+    assert _norm_err(got, ref) <= 1e-12
+    m.step(1e-4)
+    a = m.store().cpu().numpy()
+    m.load(cur)
+    m.step(1e-4)
+    assert np.array_equal(m.store().cpu().numpy(), a)
+    m.close()
+
+
+def test_async_io_dtype_conversion():
+    """store_async into an FP32 host buffer from an FP64 mesh and load_async of FP32 host data
+    into it: the same values as the blocking calls with the same conversions."""
+    import torch
+    import paper_2103_01597_b200 as b2
+    n = (40, 24, 19)
+    m, _ = _mesh(n)
+    st = synth.pcg64_state((n[2], n[1], n[0]))
+    m.load(st)
+    out32 = torch.empty((8, n[2], n[1], n[0]), dtype=torch.float32).pin_memory()
+    m.store_async(out32)
+    m.synchronize()
+    assert np.array_equal(out32.numpy(), st.astype(np.float32))
+    src32 = torch.from_numpy(st.astype(np.float32)).pin_memory()
+    m.load_async(src32)
+    m.synchronize()
+    assert np.array_equal(m.store().cpu().numpy(), st.astype(np.float32).astype(np.float64))
+    m.close()
+
+
 # ---- RHS parity ------------------------------------------------------------------------------------
 @pytest.mark.parametrize("params", [synth.P0, PSTRONG], ids=["P0", "strong"])
 @pytest.mark.parametrize("n,box", [((32, 32, 32), None), ((40, 32, 24), (2 * math.pi, 4 * math.pi, 6 * math.pi)),
