@@ -297,6 +297,12 @@ struct mhd_mesh {
   // the unsplit axes boundary slabs instead, measured 25 % slower at 4 GPUs: the extra one-tile
   // slab launches serialise on the side stream, profiles/r01/bench_iw*.json)
   bool inner_wrap = true;
+  // Several ranks: plain z-march kernels everywhere, x faces by the plain epilogue, the remote
+  // halo by a copy kernel (p2p) or pack/unpack (NCCL), y rows copied when y is unsplit
+  // (B2MHD_PLAIN=0: the storing (REMOTE) variant instead).  Measured +6 % weak 4 GPUs, +5 % weak
+  // 2 GPUs, +2 % strong 4 GPUs for p2p (profiles/r01/bench_pcopy*.json).
+  bool plain = true;
+  bool plain_ok() const { return plain && x_fits() && variant != 1 && tmaps_ok; }
   // persistent z-march schedule (one CTA per SM slot, equal plane ranges; B2MHD_PERSIST=1, one
   // rank only): measured 8 % slower than the chunked grid (11.70 vs 12.66 Gcell/s,
   // profiles/r01/bench_pers*.json) although it removes the wave tail and most chunk prologues:
@@ -563,9 +569,13 @@ bool zmarch_ok(const mhd_mesh* m, const Region& r) {
 // Periodic self-copy of the halo, only when the last update did not already write it.
 template <typename T>
 void ensure_self(mhd_mesh* m) {
-  if (m->self_list.n && !m->self_valid) {
-    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(m->self_list, sizeof(T)));
-    launch_segments<T>(m->stream, m->fields<T>(m->cur), m->g, m->self_list, SEG_SELF, nullptr);
+  // several ranks (z split, so every self segment lies in the xy plane): the x faces may already
+  // be written by the last update's epilogue (x_valid), then only the segments with a y
+  // component remain.  One rank: the whole list (its z halo is not kept by the substeps).
+  const SegList& L = m->x_valid && m->distributed() ? m->self_list_y : m->self_list;
+  if (L.n && !m->self_valid) {
+    PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(L, sizeof(T)));
+    launch_segments<T>(m->stream, m->fields<T>(m->cur), m->g, L, SEG_SELF, nullptr);
     m->launches++;
   }
   m->self_valid = true;
@@ -674,8 +684,56 @@ void p2p_halo_copy(mhd_mesh* m) {
   m->halo_valid = true;
 }
 
+// Peer-memory exchange with the plain kernel everywhere (the default; B2MHD_PLAIN=0 selects the
+// storing variant below): the boundary slabs
+// and the inner segment run the plain z-march (x faces by its predicated epilogue stores when x
+// is unsplit), and one copy kernel on the side stream then pushes the new boundary cells into
+// the neighbours' halos (the segments of P:705, all in the just-written slabs), before the
+// completion flag.  The y halo of an unsplit y axis is copied at the next substep's start.
+template <typename T>
+mhd_status substep_p2p_copy(mhd_mesh* m, int k, double dt, T* rhs_out) {
+  const bool xw = m->P[0] == 1;
+  ensure_self<T>(m);
+  if (!m->halo_valid) p2p_halo_copy<T>(m);
+  Region inner;
+  std::vector<Region> outer;
+  int thick[3];
+  slab_thickness<T>(m, thick);
+  split_regions(m, inner, outer, thick);
+  const unsigned long long s = ++m->seq;
+  CU(cudaEventRecord(m->ev_ready, m->stream));
+  CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
+  {
+    PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, 0.0);
+    launch_p2p_sync(m->comm_stream, m->peer_arrive, m->my_arrive, m->my_done, s);
+    m->launches++;
+  }
+  m->g.xwrap = !rhs_out && xw ? 1 : 0;
+  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, nullptr, m->comm_stream);
+  if (!rhs_out) {
+    const RemoteMap<T> rm = m->remote_map<T>(1 - m->cur);
+    PhaseTimer t(m, m->comm_stream, MHD_PHASE_PACK, seg_bytes(m->remote_list, sizeof(T)));
+    launch_remote_copy<T>(m->comm_stream, m->fields<T>(1 - m->cur), m->g, m->remote_list, rm);
+    m->launches++;
+  }
+  launch_p2p_signal(m->comm_stream, m->peer_done, s);
+  m->launches++;
+  CU(cudaEventRecord(m->ev_halo, m->comm_stream));
+  update_region<T>(m, inner, k, dt, rhs_out, nullptr);
+  m->g.xwrap = 0;
+  CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
+  if (!rhs_out) {
+    m->halo_valid = true;
+    m->self_valid = !m->self_list.n || (xw && !m->self_list_y.n);
+    m->x_valid = xw;
+  }
+  CU(cudaGetLastError());
+  return MHD_OK;
+}
+
 template <typename T>
 mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
+  if (m->plain_ok()) return substep_p2p_copy<T>(m, k, dt, rhs_out);
   ensure_self<T>(m);
   if (!m->halo_valid) p2p_halo_copy<T>(m);
   Region inner;
@@ -767,11 +825,14 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
   // high-priority comm stream, concurrently with the inner segment on the compute stream
   int thick[3];
   slab_thickness<T>(m, thick);
-  const bool wsplit = m->wrap_stores() && !m->inner_wrap;  // as in substep_p2p
+  const bool plain = m->plain_ok();  // plain kernels, x faces by their epilogue (see substep_p2p_copy)
+  const bool xw = plain && m->P[0] == 1;
+  const bool wsplit = !plain && m->wrap_stores() && !m->inner_wrap;  // as in substep_p2p
   split_regions(m, inner, outer, thick, wsplit);
   const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
-  const RemoteMap<T>* w = rhs_out || !m->wrap_stores() ? nullptr : &wm;
+  const RemoteMap<T>* w = rhs_out || plain || !m->wrap_stores() ? nullptr : &wm;
   const RemoteMap<T>* wi = wsplit ? nullptr : w;  // same binary as the slabs (see substep_p2p)
+  m->g.xwrap = !rhs_out && xw ? 1 : 0;
   if (m->peers.empty()) {
     update_region<T>(m, inner, k, dt, rhs_out, wi);
     for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, w);
@@ -781,7 +842,15 @@ mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
     update_region<T>(m, inner, k, dt, rhs_out, wi);
     CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
   }
-  if (!rhs_out) m->self_valid = m->wrap_stores();
+  m->g.xwrap = 0;
+  if (!rhs_out) {
+    if (plain) {
+      m->self_valid = !m->self_list.n || (xw && !m->self_list_y.n);
+      m->x_valid = xw;
+    } else {
+      m->self_valid = m->wrap_stores();
+    }
+  }
   CU(cudaGetLastError());
   return MHD_OK;
 }
@@ -931,6 +1000,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   if (const char* w = getenv("B2MHD_WRAP")) m->wrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_XWRAP")) m->xwrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_INNER_WRAP")) m->inner_wrap = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_PLAIN")) m->plain = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_PERSIST")) m->persist_env = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
   partition_xyz(info->nranks, m->P);
