@@ -21,11 +21,14 @@
 #include <string>
 #include <vector>
 
-// Wrap stores (periodic halo written by the update epilogue) vs a self-copy launch before every
-// update.  Measured (256^3 per GPU, profiles/r01/bench_wab*.json): wrap stores win with several
-// ranks (+17 % peer-memory at 4 GPUs, where the serial self-copy delayed every rank's sync; +-1 %
-// NCCL) and lose on one GPU (11.9 vs 12.4 Gcell/s: the epilogue costs more than the 0.09 ms copy),
-// so the default is "on iff nranks > 1".  B2MHD_WRAP=0/1 overrides it at mesh_create.
+// How the periodic (self) halo of unsplit axes is kept, by schedule:
+//  * one rank: z planes through the TMA plane wrap (never stored), x faces by the plain z-march
+//    epilogue (Geom::xwrap), y rows by a copy launch;
+//  * several ranks (default, plain kernels): x faces by the plain epilogue, y rows copied;
+//  * several ranks with B2MHD_PLAIN=0: "wrap stores" of the storing (REMOTE) kernel variant,
+//    which writes every self segment (and the neighbours' halos) from its epilogue.
+// Measured history in DESIGN.md 2 and profiles/r01/ (bench_wab*, bench_xw2*, bench_pcopy*).
+// B2MHD_WRAP=0/1 forces the storing-variant wrap stores off/on (on one rank too).
 
 #include "../../include/b2mhd.h"
 #include "kernels.h"
@@ -776,10 +779,10 @@ mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
   return MHD_OK;
 }
 
-// One rank: one update launch over the whole grid; its epilogue also writes the periodic halo of
-// the new state (wrap stores), so the self-copy runs only after a load.  (Overlapping a self-copy
-// with an inner segment and updating the boundary slabs on the side stream was measured slower,
-// 11.4 vs 12.4 Gcell/s at 256^3.)
+// One rank: one update launch over the whole grid (z halo by the TMA plane wrap, x faces of the
+// new state by its epilogue, y rows copied before it).  (Overlapping a self-copy with an inner
+// segment and updating the boundary slabs on the side stream was measured slower, 11.4 vs 12.4
+// Gcell/s at 256^3.)
 template <typename T>
 mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
   const Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
