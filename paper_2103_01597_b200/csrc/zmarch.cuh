@@ -62,6 +62,26 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 // refills the ring.  Measured (256^3, one B200): +15 % for the FP64 order-8 kernel (32x4 tile,
 // 4 warps per SM); slower with 8 warps per SM (-12 % FP64 / -17 % FP32 at order 6, -15 % FP32 at
 // order 8), so only the 4-row tiles use it.
+#ifndef B2_ZM_TQ
+#define B2_ZM_TQ 0
+#endif
+// tensor-memory z queue helpers (ZCfg::TQ)
+__device__ __forceinline__ void tq_ld4(unsigned addr, double (&v)[4]) {
+  unsigned r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+__device__ __forceinline__ void tq_st1(unsigned addr, double v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(addr),
+               "r"((unsigned)__double2loint(v)), "r"((unsigned)__double2hiint(v))
+               : "memory");
+}
+__device__ __forceinline__ void tq_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
 __device__ __forceinline__ void bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
@@ -86,9 +106,13 @@ struct ZCfg {
   static constexpr int PSZ = (TY * PCOLS * ES + 127) / 128 * 128 / ES;  // f_{k-1} tile per field
   static constexpr unsigned HALO_TX = (unsigned)(NF * ROWS * COLS * ES);
   static constexpr unsigned PREV_TX = (unsigned)(NF * TY * PCOLS * ES);
-  static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128;
+  static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128 + 16;
   static constexpr bool FITS = SMEM <= 227 * 1024;
   static constexpr bool SKEW = TY < 8;  // the 4-row tiles (FP64, r = 4)
+  // z queue in tensor memory (B2_ZM_TQ): the centres of planes o..o+2 of every field are kept per
+  // thread in TMEM (tcgen05.st / tcgen05.ld, 32x32b shape) instead of being re-read from the ring
+  // as the z taps of three successive outputs (FP64, r = 3)
+  static constexpr bool TQ = B2_ZM_TQ && sizeof(T) == 8 && RAD == 3 && !SKEW;
 };
 
 // Register state carried along z by one thread.
@@ -109,6 +133,52 @@ struct ZStep {
   int slot0;  // plane zb - r (first staged plane) has slot 0
   const RemoteMap<T>& rm;
   bool lead;  // leading warp group (ZCfg::SKEW): signals "past the loads of plane o" mid-iteration
+  unsigned tq;  // ZCfg::TQ: tensor-memory address of this thread's z queue (lane, column group)
+
+  // queue slot of plane o + i at phase PH is (i + PH) % 3; field q owns columns 8q .. 8q + 5
+  template <int PH>
+  __device__ __forceinline__ void zq_get(int q, T (&z)[3]) const {
+    double v[4];
+    tq_ld4(tq + 8u * (unsigned)q, v);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) z[i] = v[(i + PH) % 3];
+  }
+  template <int PH>
+  __device__ __forceinline__ void zq_put(int q, T val) const {
+    tq_st1(tq + 8u * (unsigned)q + 2u * (unsigned)(PH % 3), val);
+  }
+  // z derivatives of field q at output o from the queue (o, o+1, o+2), the ring (o+3) and the
+  // register history (o-3 .. o-1); the same arithmetic as axis_z
+  template <int PH>
+  __device__ __forceinline__ void axis_zq(const March<T, RAD>& st, int q, T f0, const T (&zp)[RAD], T& d1,
+                                          T& d2) const {
+    T dl[RAD], sg[RAD];
+#pragma unroll
+    for (int i = 1; i <= RAD; ++i) {
+      const T p = zp[i - 1], m = st.hist[q][(RAD - i + PH) % RAD];
+      dl[i - 1] = p - m;
+      sg[i - 1] = p + m;
+    }
+    d1 = d1_of<T, RAD>(dl, C.c1[2]);
+    d2 = d2_of<T, RAD>(f0, sg, C.d2[2], C.d0[2]);
+  }
+  // centre of field q at output plane o, with its z derivatives; pushes plane o+3 into the queue
+  template <int PH>
+  __device__ __forceinline__ T centre_z(const March<T, RAD>& st, int q, const T* const (&sk)[RAD + 1], T& d1,
+                                        T& d2) const {
+    if constexpr (Z::TQ) {
+      T z[3];
+      zq_get<PH>(q, z);
+      const T zp[RAD] = {z[1], z[2], at(sk[RAD], q, 0, 0)};
+      zq_put<PH>(q, zp[RAD - 1]);
+      axis_zq<PH>(st, q, z[0], zp, d1, d2);
+      return z[0];
+    } else {
+      const T f0 = at(sk[0], q, 0, 0);
+      axis_z<PH>(st, q, f0, sk, d1, d2);
+      return f0;
+    }
+  }
 
   __device__ __forceinline__ void signal_half(int o) const {
     if (Z::SKEW && lead) bar_arrive(1 + (o & 1), Z::NT);
@@ -204,6 +274,11 @@ struct ZStep {
     }
 #pragma unroll
     for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % RAD] = at(s0, q, 0, 0);
+    if constexpr (Z::TQ) {
+      const T* s3 = slot_of(p + RAD);
+#pragma unroll
+      for (int q = 0; q < NF; ++q) zq_put<PH>(q, at(s3, q, 0, 0));
+    }
     signal_half(p);
   }
 
@@ -218,14 +293,19 @@ struct ZStep {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const int q = qx + c;
-      f[c] = at(s0, q, 0, 0);
       T d1a[2], d2a[2];
-      axis_xy(s0, q, f[c], d1a, d2a, dlx[c], dly[c]);
+      if constexpr (Z::TQ) {
+        f[c] = centre_z<PH>(st, q, sk, g[c][2], d2[c][2]);
+        axis_xy(s0, q, f[c], d1a, d2a, dlx[c], dly[c]);
+      } else {
+        f[c] = at(s0, q, 0, 0);
+        axis_xy(s0, q, f[c], d1a, d2a, dlx[c], dly[c]);
+        axis_z<PH>(st, q, f[c], sk, g[c][2], d2[c][2]);
+      }
       g[c][0] = d1a[0];
       g[c][1] = d1a[1];
       d2[c][0] = d2a[0];
       d2[c][1] = d2a[1];
-      axis_z<PH>(st, q, f[c], sk, g[c][2], d2[c][2]);
     }
     // graddiv cross parts: k < 0 (accumulated), + in-plane part at k = 0, then k = 1..r
     const T P0 = cross_xy_s(s0, qx + 1);  // d_x d_y v_y
@@ -266,10 +346,15 @@ struct ZStep {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int q = h == 0 ? LNRHO : SS;
-      sc[h] = at(sk[0], q, 0, 0);
       T d1a[2], d2a[2], dlx[RAD], dly[RAD], d2z;
-      axis_xy(sk[0], q, sc[h], d1a, d2a, dlx, dly);
-      axis_z<PH>(st, q, sc[h], sk, gsc[h][2], d2z);
+      if constexpr (Z::TQ) {
+        sc[h] = centre_z<PH>(st, q, sk, gsc[h][2], d2z);
+        axis_xy(sk[0], q, sc[h], d1a, d2a, dlx, dly);
+      } else {
+        sc[h] = at(sk[0], q, 0, 0);
+        axis_xy(sk[0], q, sc[h], d1a, d2a, dlx, dly);
+        axis_z<PH>(st, q, sc[h], sk, gsc[h][2], d2z);
+      }
       gsc[h][0] = d1a[0];
       gsc[h][1] = d1a[1];
       lap[h] = (d2a[0] + d2a[1]) + d2z;
@@ -344,6 +429,20 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     for (int s = 0; s < Z::NSLOT; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  unsigned tq = 0;
+  if constexpr (Z::TQ) {
+    // 128 TMEM columns: 2 column groups (warps w and w + 4 share a lane quadrant) x 8 fields x 8
+    uint32_t* const tbase = reinterpret_cast<uint32_t*>(mbar + Z::NSLOT);
+    if (tid < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_u32(tbase)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const int warp = tid / 32;
+    tq = *tbase + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)((warp >> 2) * 64);
+  }
   __syncthreads();
 
   // One segment: the tile column at (x0, y0), output planes [zb, ze).  `base` = planes this CTA
@@ -379,7 +478,7 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     };
 
     const ZStep<T, RAD, MODE, REMOTE> S{ring, prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
-                                        first - (int)(base % Z::NSLOT), rm, lead};
+                                        first - (int)(base % Z::NSLOT), rm, lead, tq};
     March<T, RAD> st;
 #pragma unroll
     for (int v = 0; v < 2; ++v)
@@ -407,6 +506,7 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
         issue(p + RAD + 1);
       }
       wait_plane(p + RAD);  // plane p+r and f_{k-1}(p) have landed
+      if constexpr (Z::TQ) tq_wait_st();  // last iteration's queue store is visible to its loads
       if (p < zb)
         S.template push_only<PH>(st, p);
       else
@@ -440,6 +540,16 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     base += (unsigned)(zlen + 2 * RAD);
     u += zlen;
     if (u < u1) __syncthreads();  // every thread is done with the ring before the next prologue
+  }
+  if constexpr (Z::TQ) {
+    tq_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t* const tbase = reinterpret_cast<uint32_t*>(mbar + Z::NSLOT);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(*tbase));
+    }
   }
   if (REMOTE && rm.sys) __threadfence_system();  // peer halo stores visible before the completion signal
 }
