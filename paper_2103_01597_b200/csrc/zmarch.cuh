@@ -71,14 +71,16 @@ __device__ __forceinline__ void tq_ld4(unsigned addr, double (&v)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(addr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  // the wait is tied to the loaded registers (not a memory clobber), so that the compiler may
+  // still move shared-memory loads across it
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
 #pragma unroll
   for (int i = 0; i < 4; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
 }
 __device__ __forceinline__ void tq_st1(unsigned addr, double v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(addr),
-               "r"((unsigned)__double2loint(v)), "r"((unsigned)__double2hiint(v))
-               : "memory");
+               "r"((unsigned)__double2loint(v)), "r"((unsigned)__double2hiint(v)));
 }
 __device__ __forceinline__ void tq_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
