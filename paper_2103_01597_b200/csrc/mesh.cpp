@@ -666,9 +666,9 @@ void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer,
 template <typename T>
 void slab_thickness(const mhd_mesh* m, int thick[3]) {
   thick[0] = zm_tx<T>();
-  // one tile row: 8, or 16 for the FP32 order-6 tile (an 8-row slab would leave half of every
-  // 16-row tile idle)
-  thick[1] = (sizeof(T) == 4 && m->info.radius == 3) ? zm_ty<T, 3>() : 8;
+  // 8 rows (for the 16-row FP32 order-6 tile a 16-row slab measured the same: 65.0 vs 65.8
+  // Gcell/s at 4 GPUs, profiles/r01/bench_f32s_*.json)
+  thick[1] = 8;
   thick[2] = m->exchange == 1 ? 16 : 8;
   if (m->slab_env[0] > 0)
     for (int a = 0; a < 3; ++a) thick[a] = m->slab_env[a];
