@@ -313,6 +313,11 @@ struct mhd_mesh {
   // rows they share stop hitting in L2.  Off by default.
   bool persist = false;
   int persist_env = -1;
+  // z chunk of the boundary-slab launches on the side stream: 16 planes for FP32 (more, shorter
+  // CTAs shorten the slab chain, which is the critical path next to the fast FP32 inner segment:
+  // 65.3 -> 82.7 Gcell/s at 4 GPUs), the default 64 for FP64 (16: -2 %; profiles/r01/bench_szc*).
+  // B2MHD_SLAB_ZCHUNK=n overrides (0: 64).
+  int slab_zchunk = -1;
   ncclComm_t comm = nullptr;
   int cur = 0;
   int next_k = 0;
@@ -539,7 +544,8 @@ void update_region_r(mhd_mesh* m, cudaStream_t st, const Region& r, int k, doubl
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
   PhaseTimer t(m, st, st == m->stream ? MHD_PHASE_UPDATE : MHD_PHASE_OUTER, cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
   if (zm)
-    launch_zmarch<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, rm, m->persist);
+    launch_zmarch<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, rm, m->persist,
+                          st == m->stream ? 0 : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 0)));
   else
     launch_direct<T, RAD>(st, in, out, m->g, r, C, k, rhs_out, rm);
   m->launches++;
@@ -1007,6 +1013,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   if (const char* w = getenv("B2MHD_INNER_WRAP")) m->inner_wrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_PLAIN")) m->plain = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_PERSIST")) m->persist_env = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_SLAB_ZCHUNK")) m->slab_zchunk = atoi(w);
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
   partition_xyz(info->nranks, m->P);
   coord_xyz(info->rank, m->coord);

@@ -560,7 +560,7 @@ constexpr int kNZC = 64;
 
 template <typename T, int RAD, int MODE, bool REMOTE>
 void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm, bool persist) {
+                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm, bool persist, int zchunk) {
   using Z = ZCfg<T, RAD>;
   static int resident = 0;  // CTAs of this instantiation that fit on the GPU at once
   if (!resident) {
@@ -572,7 +572,8 @@ void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, zmarch_kernel<T, RAD, MODE, REMOTE>, Z::NT, Z::SMEM);
     resident = std::max(1, sms * std::max(1, per));
   }
-  const int nzc = r.ext[2] < kNZC ? r.ext[2] : kNZC;
+  const int cz = zchunk > 0 ? zchunk : kNZC;
+  const int nzc = r.ext[2] < cz ? r.ext[2] : cz;
   dim3 grd((r.ext[0] + Z::TX - 1) / Z::TX, (r.ext[1] + Z::TY - 1) / Z::TY, (r.ext[2] + nzc - 1) / nzc);
   // persistent schedule when the chunked grid would take more than one wave (and the warp-group
   // skew, whose barrier ids follow the plane parity, is off)
@@ -591,21 +592,22 @@ bool zmarch_supported(const Geom& g, const Region& r) {
 
 template <typename T, int RAD>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm, bool persist) {
+                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm, bool persist,
+                   int zchunk) {
   if constexpr (zm::ZCfg<T, RAD>::FITS) {
     RemoteMap<T> none;
     if (rhs_out)
-      zm::launch_cfg<T, RAD, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none, persist);
+      zm::launch_cfg<T, RAD, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none, persist, zchunk);
     else if (rm)
-      zm::launch_cfg<T, RAD, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm, persist);
+      zm::launch_cfg<T, RAD, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm, persist, zchunk);
     else
-      zm::launch_cfg<T, RAD, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none, persist);
+      zm::launch_cfg<T, RAD, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none, persist, zchunk);
   }
 }
 
 #define B2_ZMARCH_INSTANTIATE(T, RAD)                                                                      \
   template bool zmarch_supported<T, RAD>(const Geom&, const Region&);                                       \
   template void launch_zmarch<T, RAD>(cudaStream_t, const TmapSet&, const Fields<T>&, const Geom&, const Region&, \
-                                      const Coef<T>&, int, T*, int, const RemoteMap<T>*, bool);
+                                      const Coef<T>&, int, T*, int, const RemoteMap<T>*, bool, int);
 
 }  // namespace b2
