@@ -59,7 +59,8 @@ def parse():
 
 # ---- clocks during the timed region (B200_PROFILING.md clocks line) -------------------------------
 class ClockSampler:
-    """SM clock, power and throttle reasons sampled every 20 ms by NVML while the timed region runs."""
+    """SM and memory clocks, power and throttle reasons sampled every 20 ms by NVML while the timed
+    region runs (NVML is initialised before the region so that sampling starts with it)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
@@ -70,18 +71,27 @@ class ClockSampler:
         self.stop = threading.Event()
         self.t = threading.Thread(target=self.run, daemon=True)
         self.err = None
-
-    def run(self):
+        self.h = None
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def run(self):
+        if self.h is None:
+            return
+        nv = self.nv
+        try:
             while not self.stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, mx, pw, rs))
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                mem = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_MEM)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, self.mx, pw, rs, mem))
                 self.stop.wait(0.02)
         except Exception as e:  # pragma: no cover
             self.err = str(e)
@@ -99,6 +109,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: %s" % self.err]}
         reasons = sorted({n for s in self.samples for n, bit in self.REASONS.items() if s[3] & bit})
         return {"sm_mhz": statistics.median(s[0] for s in self.samples), "sm_max_mhz": max(s[1] for s in self.samples),
+                "mem_mhz": statistics.median(s[4] for s in self.samples),
                 "power_w_max": max(s[2] for s in self.samples), "samples": len(self.samples), "reasons": reasons}
 
 
