@@ -113,6 +113,24 @@ class ClockSampler:
                 "power_w_max": max(s[2] for s in self.samples), "samples": len(self.samples), "reasons": reasons}
 
 
+def numa_bind(gpu_index: int) -> None:
+    """N > 1: run this rank on the host cores next to its GPU (NVML CPU affinity), so that its
+    pinned host buffers are first touched on the GPU's own NUMA node; the end-to-end copies of
+    several ranks then do not cross the socket interconnect.  (N = 1 keeps every core for the
+    CPU baseline.)"""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+    except Exception:
+        pass
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -221,6 +239,8 @@ def main():
     import paper_2103_01597_b200 as b2
 
     torch.cuda.set_device(local)
+    if world > 1:
+        numa_bind(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
