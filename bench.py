@@ -59,8 +59,9 @@ def parse():
 
 # ---- clocks during the timed region (B200_PROFILING.md clocks line) -------------------------------
 class ClockSampler:
-    """SM and memory clocks, power and throttle reasons sampled every 20 ms by NVML while the timed
-    region runs (NVML is initialised before the region so that sampling starts with it)."""
+    """SM clock, power and throttle reasons sampled every 20 ms by NVML while the timed region
+    runs; the memory clock is read once at the end (a per-sample memory-clock query measurably
+    slowed the launch-heavy multi-GPU schedule)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
@@ -71,28 +72,21 @@ class ClockSampler:
         self.stop = threading.Event()
         self.t = threading.Thread(target=self.run, daemon=True)
         self.err = None
-        self.h = None
+        self.mem = None
+
+    def run(self):
         try:
             import pynvml
             pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception as e:  # pragma: no cover
-            self.err = str(e)
-
-    def run(self):
-        if self.h is None:
-            return
-        nv = self.nv
-        try:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             while not self.stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                mem = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_MEM)
-                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((sm, self.mx, pw, rs, mem))
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, mx, pw, rs))
                 self.stop.wait(0.02)
+            self.mem = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_MEM)
         except Exception as e:  # pragma: no cover
             self.err = str(e)
 
@@ -109,8 +103,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: %s" % self.err]}
         reasons = sorted({n for s in self.samples for n, bit in self.REASONS.items() if s[3] & bit})
         return {"sm_mhz": statistics.median(s[0] for s in self.samples), "sm_max_mhz": max(s[1] for s in self.samples),
-                "mem_mhz": statistics.median(s[4] for s in self.samples),
-                "power_w_max": max(s[2] for s in self.samples), "samples": len(self.samples), "reasons": reasons}
+                "mem_mhz_end": self.mem, "power_w_max": max(s[2] for s in self.samples), "samples": len(self.samples),
+                "reasons": reasons}
 
 
 def numa_bind(gpu_index: int) -> None:
