@@ -71,3 +71,17 @@ def test_row_wise_vs_morton_internode_faces():
     row = collections.Counter(perfmodel.internode_faces((16, 16, 16), 8, "row"))
     mor = collections.Counter(perfmodel.internode_faces((16, 16, 16), 8, "morton"))
     assert set(row) == {4, 5} and mor == {3: 4096}
+
+
+def test_ulp_metric_eqs_15_16():
+    """Eqs. 15-16 (P:899-907): eps = 2^(floor(log2|m|) - p + 1), error = |m - c| / eps, p = 53.
+    Pinned with values whose spacing is known exactly (numpy.spacing)."""
+    import numpy as np
+    import ulp_check
+    m = np.array([1.0, 1.5, 0.75, 1e-3, -3.0, 2.0 ** -30])
+    for k in (0, 1, 3):
+        c = m + k * np.spacing(np.abs(m)) * np.sign(m)
+        u, z = ulp_check.ulp_errors(m, c)
+        assert np.array_equal(u, np.full(m.size, float(k))) and z.size == 0
+    u, z = ulp_check.ulp_errors(np.array([0.0, 1.0]), np.array([1e-30, 1.0]))
+    assert u.tolist() == [0.0] and z.tolist() == [1e-30]
