@@ -21,7 +21,12 @@
  *   - All device work of a mesh is issued on the CUDA stream passed to
  *     mhd_mesh_create (internal comm streams join it with events).  Calls are
  *     asynchronous with respect to the host unless documented as blocking.
- *   - One mesh per host thread; one process per GPU (torchrun).
+ *   - One mesh per host thread.  Ranks run one process per GPU (torchrun; the NCCL or
+ *     peer-memory exchange), or several ranks in one process (mhd_group_*, for fewer GPUs
+ *     than ranks or a single-process driver).
+ *   - Where a call has no passage of its own, the reading it implements is SURVEY §8(b)
+ *     ("the field state loaded and stored per rank", "an ISL iteration = halo exchange +
+ *     update", "verification by comparing stored state") over the problem statement P:194-212.
  */
 #ifndef B2MHD_H
 #define B2MHD_H
@@ -34,7 +39,8 @@ extern "C" {
 #endif
 
 #define MHD_ABI_VERSION 1
-#define MHD_RADIUS 3      /* stencil radius r (Eq. 1); 6th order: k = 2r */
+#define MHD_RADIUS 3      /* default stencil radius r (Eq. 1); 6th order: k = 2r.
+                             mhd_mesh_info.radius may be 1..4 (orders 2, 4, 6, 8) */
 #define MHD_NSEGMENTS 26  /* 6 sides + 12 edges + 8 corners */
 
 typedef enum {
@@ -42,7 +48,7 @@ typedef enum {
   MHD_EINVAL = 1,       /* bad argument (null pointer, field index, k out of range, ...) */
   MHD_EDECOMP = 2,      /* p_i does not divide n_i, or nranks is not a power of two */
   MHD_ESMALL = 3,       /* local extent n'_i <= 2r: no inner segment */
-  MHD_EUNSUPPORTED = 4, /* radius != 3, unknown dtype, ABI version mismatch */
+  MHD_EUNSUPPORTED = 4, /* radius outside 1..4, unknown dtype, ABI version mismatch, > 7 neighbours */
   MHD_ECUDA = 5,        /* a CUDA runtime call failed */
   MHD_ENCCL = 6,        /* an NCCL call failed, or comm used before mhd_comm_init */
   MHD_ENOMEM = 7,       /* workspace smaller than mhd_workspace_bytes */
@@ -77,7 +83,7 @@ typedef struct {
 typedef struct {
   int32_t abi_version;      /* must be MHD_ABI_VERSION */
   int64_t n[3];             /* global computational domain N (x, y, z) */
-  int32_t radius;           /* must be MHD_RADIUS */
+  int32_t radius;           /* stencil radius r = 1..4 (order 2r); MHD_RADIUS = 3 is the paper's */
   double ds[3];             /* grid spacing (x, y, z) */
   int32_t dtype;            /* mhd_dtype */
   int32_t rank, nranks;     /* this process and C_P; C_P a power of two */
@@ -91,7 +97,7 @@ typedef struct mhd_mesh mhd_mesh; /* opaque */
  * offset o in {-1,0,1}^3 \ {0}.  The rank RECEIVES dst region (halo cells at
  * offset o) from recv_peer = rank of coord + o, and SENDS src region (its own
  * interior cells that neighbour coord - o needs) to send_peer.  Coordinates are
- * interior-relative: 0 .. n'-1 is the interior, -3 .. -1 and n' .. n'+2 the halo.
+ * interior-relative: 0 .. n'-1 is the interior, -r .. -1 and n' .. n'+r-1 the halo.
  * Segments to one peer are concatenated in canonical order (sides, edges,
  * corners; lexicographic offset within a class) at buffer offsets in cells. */
 typedef struct {
@@ -114,20 +120,26 @@ mhd_status mhd_decompose(const mhd_mesh_info* info, int32_t rank, int32_t P[3],
 mhd_status mhd_segment_table(const mhd_mesh_info* info, int32_t rank, mhd_segment* out,
                              int32_t max_segments, int32_t* count);
 
-/* Bytes of device workspace a mesh needs (two pitched states + comm buffers). */
+/* Bytes of device workspace a mesh needs: two pitched states (8 fields of (n'+2r)^3 cells, R#4:
+ * f_k and f_{k-1}), the send/recv buffers of the P:705 segments, reduction scratch and the
+ * peer-memory flags.  Pure host function. */
 mhd_status mhd_workspace_bytes(const mhd_mesh_info* info, size_t* bytes);
 
 /* ---- mesh lifecycle ------------------------------------------------------ */
 
-/* dev_workspace: caller-owned device memory of >= mhd_workspace_bytes, borrowed
+/* The subdomain of `rank` on the current CUDA device.
+ * dev_workspace: caller-owned device memory of >= mhd_workspace_bytes, borrowed
  * until mhd_mesh_destroy.  cuda_stream: a cudaStream_t (0 = legacy default).
  * Checks divisibility (EDECOMP), n'_i > 2r (ESMALL), radius/dtype (EUNSUPPORTED).
- * The state is zero after create. */
+ * The state is zero after create.  Environment knobs read here (A/B measurements only):
+ * B2MHD_XWRAP, B2MHD_PERSIST, B2MHD_SLAB, B2MHD_SLAB_ZCHUNK, B2MHD_POISON (= mhd_set_debug),
+ * B2MHD_SPIN_TIMEOUT_S (peer-memory flag waits, default 60 s). */
 mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_t bytes,
                            void* cuda_stream, mhd_mesh** out);
 
-/* Multi-GPU only: nccl_unique_id is the 128-byte ncclUniqueId created by rank 0
- * (mhd_nccl_unique_id) and broadcast by the caller.  Collective over all ranks. */
+/* Multi-GPU, one process per rank (the paper's MPI ranks): nccl_unique_id is the
+ * 128-byte ncclUniqueId created by rank 0 (mhd_nccl_unique_id) and broadcast by the caller.
+ * Collective over all ranks.  Needed for reductions and the NCCL exchange. */
 mhd_status mhd_nccl_unique_id(void* out128);
 mhd_status mhd_comm_init(mhd_mesh* mesh, const void* nccl_unique_id);
 
@@ -136,24 +148,33 @@ mhd_status mhd_comm_init(mhd_mesh* mesh, const void* nccl_unique_id);
  * blobs in rank order and passes them to mhd_p2p_open (collective, after every rank created its
  * mesh; follow it with a host barrier).  From then on the outer-shell update kernels store their
  * boundary results directly into the neighbours' halos (no pack, send/recv or unpack), ordered by
- * system-scope flags in the workspaces.  mhd_set_exchange(mesh, 0) returns to NCCL. */
+ * system-scope flags in the workspaces (the paper's P:765-782 pipeline without the
+ * pack/unpack copies).  Ranks must call the same substeps in lockstep; a flag wait that outlasts
+ * B2MHD_SPIN_TIMEOUT_S gives up and the next blocking call (mhd_synchronize, mhd_store to host,
+ * mhd_reduce) returns MHD_ECUDA.  mhd_set_exchange(mesh, 0) returns to NCCL. */
 #define MHD_P2P_HANDLE_BYTES 80
 mhd_status mhd_p2p_export(mhd_mesh* mesh, void* out_blob);
 mhd_status mhd_p2p_open(mhd_mesh* mesh, const void* blobs);
 mhd_status mhd_set_exchange(mhd_mesh* mesh, int32_t mode); /* 0: NCCL, 1: peer memory */
 
+/* Releases the mesh (not the caller's workspace).  With the peer-memory exchange it first waits
+ * until the neighbours' stores of their last operation into this workspace have landed; the
+ * caller should also barrier across ranks before freeing the workspace.  A mesh in a group:
+ * MHD_EINVAL until mhd_group_destroy. */
 mhd_status mhd_mesh_destroy(mhd_mesh* mesh);
 
 /* ---- state I/O ------------------------------------------------------------ */
 
 /* Copy a local interior buffer into the current state (converting dtype if it
  * differs from the mesh dtype).  Resets the RK3 substep counter to 0: a loaded
- * state is a step boundary, where the 2N register w is zero (alpha_0 = 0). */
+ * state is a step boundary, where the 2N register w is zero (alpha_0 = 0, R#3).
+ * The paper's initial condition is random values in [0, 1] loaded per rank. */
 mhd_status mhd_load(mhd_mesh* mesh, int32_t field, const void* src, int32_t src_dtype,
                     int32_t on_device);
 
-/* Copy the current state's local interior into dst.  Blocking when
- * on_device == 0 (synchronises the mesh stream); see mhd_store_async. */
+/* Copy the current state's local interior into dst (the paper verifies by comparing stored
+ * state against the CPU model).  Blocking when on_device == 0 (synchronises the mesh
+ * stream); see mhd_store_async. */
 mhd_status mhd_store(mhd_mesh* mesh, int32_t field, void* dst, int32_t dst_dtype,
                      int32_t on_device);
 
@@ -185,7 +206,8 @@ mhd_status mhd_store_grid(mhd_mesh* mesh, int32_t field, void* dst, int32_t on_d
 /* ---- the hot path ---------------------------------------------------------- */
 
 /* Fill the halo of the current state: periodic along unsplit axes, and
- * the 26-segment exchange with neighbours.  Bit-exact copies. */
+ * the 26-segment exchange with neighbours.  Bit-exact copies.
+ * A mesh in a group: MHD_EINVAL (use mhd_group_halo_exchange). */
 mhd_status mhd_halo_exchange(mhd_mesh* mesh);
 
 /* One ISL iteration = RK3 substep k: halo exchange overlapped
@@ -209,7 +231,9 @@ mhd_status mhd_reduce(mhd_mesh* mesh, int32_t field, int32_t op, double* out);
  * halo exchange first.  Does not change the state or the substep counter. */
 mhd_status mhd_debug_rhs(mhd_mesh* mesh, void* dev_dst);
 
-/* Block the host until all work of the mesh has completed. */
+/* Block the host until all work of the mesh has completed (the per-iteration device
+ * synchronisation of P:782, which the substeps themselves replace by stream order).  Reports a
+ * timed-out peer-memory flag wait (MHD_ECUDA). */
 mhd_status mhd_synchronize(mhd_mesh* mesh);
 
 /* ---- configuration and introspection --------------------------------------- */
@@ -221,6 +245,13 @@ mhd_status mhd_set_kernel(mhd_mesh* mesh, int32_t variant);
 /* Local geometry of the mesh: P, coord, local n', and the substep counter. */
 mhd_status mhd_mesh_query(const mhd_mesh* mesh, int32_t P[3], int32_t coord[3],
                           int64_t local_n[3], int32_t* next_k);
+
+/* Debug flags.  MHD_DEBUG_POISON_HALO: before every update, every halo cell of the state the
+ * update writes (and, at load, of the loaded field) is set to NaN, so that a stencil reading a
+ * halo cell the schedule did not refresh (e.g. a corner, which P:937 says is never needed)
+ * produces NaN.  Results are bit-identical with and without it when the schedule is right. */
+#define MHD_DEBUG_POISON_HALO 1
+mhd_status mhd_set_debug(mhd_mesh* mesh, int32_t flags);
 
 /* Number of kernels the library launched on this mesh since create. */
 mhd_status mhd_launch_count(const mhd_mesh* mesh, int64_t* count);
@@ -247,6 +278,29 @@ mhd_status mhd_profile_enable(mhd_mesh* mesh, int32_t enable);
  * cells x 8 fields x sizeof(T) x 2). */
 mhd_status mhd_profile_read(mhd_mesh* mesh, int32_t phase, int64_t* launches, double* ms,
                             double* algorithmic_bytes);
+
+/* ---- several ranks in one process ---------------------------------------------------------
+ * A group drives every rank of an n-rank decomposition from one host thread: meshes created
+ * with nranks = n and rank = 0..n-1 (each on the CUDA device current at its create; several on
+ * one device allowed), passed in rank order, without mhd_comm_init / mhd_p2p_open.  The same
+ * schedules and kernels run as with one process per rank; the transfer of
+ * exchange = 0 is a copy-engine pull of each neighbour's packed send buffer (cudaMemcpyAsync)
+ * instead of NCCL, exchange = 1 the peer-memory stores, and cross-rank ordering uses CUDA events
+ * recorded phase by phase across the ranks, so no kernel waits on another.  While grouped, the
+ * per-mesh hot-path calls return MHD_EINVAL; load/store/store_grid stay per mesh.  Peer access is
+ * enabled between the devices of neighbouring ranks. */
+typedef struct mhd_group mhd_group; /* opaque */
+mhd_status mhd_group_create(mhd_mesh* const* meshes, int32_t n, int32_t exchange, mhd_group** out);
+mhd_status mhd_group_halo_exchange(mhd_group* group);
+mhd_status mhd_group_integrate_substep(mhd_group* group, int32_t k, double dt);
+mhd_status mhd_group_integrate_step(mhd_group* group, double dt);
+/* dev_dst[i]: the RHS destination of rank i, as mhd_debug_rhs. */
+mhd_status mhd_group_debug_rhs(mhd_group* group, void* const* dev_dst);
+/* Global reduction: per-rank partials combined on the host in rank order. */
+mhd_status mhd_group_reduce(mhd_group* group, int32_t field, int32_t op, double* out);
+mhd_status mhd_group_synchronize(mhd_group* group);
+/* Synchronises every rank and releases the grouping (not the meshes). */
+mhd_status mhd_group_destroy(mhd_group* group);
 
 const char* mhd_status_str(mhd_status s);
 const char* mhd_last_error(void);

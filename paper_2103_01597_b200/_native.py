@@ -24,8 +24,11 @@ STATUS = {0: "MHD_OK", 1: "MHD_EINVAL", 2: "MHD_EDECOMP", 3: "MHD_ESMALL", 4: "M
 SYMBOLS = ("mhd_decompose", "mhd_segment_table", "mhd_workspace_bytes", "mhd_mesh_create", "mhd_nccl_unique_id",
            "mhd_comm_init", "mhd_p2p_export", "mhd_p2p_open", "mhd_set_exchange", "mhd_mesh_destroy", "mhd_load", "mhd_store", "mhd_store_async", "mhd_load_async", "mhd_store_grid", "mhd_halo_exchange",
            "mhd_integrate_substep", "mhd_integrate_step", "mhd_reduce", "mhd_debug_rhs", "mhd_synchronize",
-           "mhd_set_kernel", "mhd_mesh_query", "mhd_launch_count", "mhd_profile_enable", "mhd_profile_read", "mhd_status_str", "mhd_last_error",
-           "mhd_abi_version")
+           "mhd_set_kernel", "mhd_set_debug", "mhd_mesh_query", "mhd_launch_count", "mhd_profile_enable", "mhd_profile_read",
+           "mhd_group_create", "mhd_group_halo_exchange", "mhd_group_integrate_substep", "mhd_group_integrate_step",
+           "mhd_group_debug_rhs", "mhd_group_reduce", "mhd_group_synchronize", "mhd_group_destroy",
+           "mhd_status_str", "mhd_last_error", "mhd_abi_version")
+MHD_DEBUG_POISON_HALO = 1
 
 
 class MhdError(RuntimeError):
@@ -79,6 +82,15 @@ def _load():
         "mhd_debug_rhs": [ctypes.c_void_p, ctypes.c_void_p],
         "mhd_synchronize": [ctypes.c_void_p],
         "mhd_set_kernel": [ctypes.c_void_p, ctypes.c_int32],
+        "mhd_set_debug": [ctypes.c_void_p, ctypes.c_int32],
+        "mhd_group_create": [P(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int32, P(ctypes.c_void_p)],
+        "mhd_group_halo_exchange": [ctypes.c_void_p],
+        "mhd_group_integrate_substep": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_double],
+        "mhd_group_integrate_step": [ctypes.c_void_p, ctypes.c_double],
+        "mhd_group_debug_rhs": [ctypes.c_void_p, P(ctypes.c_void_p)],
+        "mhd_group_reduce": [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, P(ctypes.c_double)],
+        "mhd_group_synchronize": [ctypes.c_void_p],
+        "mhd_group_destroy": [ctypes.c_void_p],
         "mhd_mesh_query": [ctypes.c_void_p, P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int64), P(ctypes.c_int32)],
         "mhd_launch_count": [ctypes.c_void_p, P(ctypes.c_int64)],
         "mhd_profile_enable": [ctypes.c_void_p, ctypes.c_int32],
@@ -239,6 +251,51 @@ def mhd_synchronize(mesh: int) -> None:
 
 def mhd_set_kernel(mesh: int, variant: int) -> None:
     check(lib.mhd_set_kernel(ctypes.c_void_p(mesh), variant), "mhd_set_kernel")
+
+
+def mhd_set_debug(mesh: int, flags: int) -> None:
+    check(lib.mhd_set_debug(ctypes.c_void_p(mesh), flags), "mhd_set_debug")
+
+
+# ---- several ranks in one process ----
+def mhd_group_create(meshes, exchange: int) -> int:
+    arr = (ctypes.c_void_p * len(meshes))(*meshes)
+    g = ctypes.c_void_p()
+    check(lib.mhd_group_create(arr, len(meshes), exchange, ctypes.byref(g)), "mhd_group_create")
+    return g.value
+
+
+def mhd_group_halo_exchange(group: int) -> None:
+    check(lib.mhd_group_halo_exchange(ctypes.c_void_p(group)), "mhd_group_halo_exchange")
+
+
+def mhd_group_integrate_substep(group: int, k: int, dt: float) -> None:
+    check(lib.mhd_group_integrate_substep(ctypes.c_void_p(group), k, dt), "mhd_group_integrate_substep")
+
+
+def mhd_group_integrate_step(group: int, dt: float) -> None:
+    check(lib.mhd_group_integrate_step(ctypes.c_void_p(group), dt), "mhd_group_integrate_step")
+
+
+def mhd_group_debug_rhs(group: int, dev_ptrs) -> None:
+    arr = (ctypes.c_void_p * len(dev_ptrs))(*dev_ptrs)
+    check(lib.mhd_group_debug_rhs(ctypes.c_void_p(group), arr), "mhd_group_debug_rhs")
+
+
+def mhd_group_reduce(group: int, field: int, op: int, allow_nonfinite: bool = False) -> float:
+    out = ctypes.c_double()
+    st = lib.mhd_group_reduce(ctypes.c_void_p(group), field, op, ctypes.byref(out))
+    if not (allow_nonfinite and st == 8):
+        check(st, "mhd_group_reduce")
+    return out.value
+
+
+def mhd_group_synchronize(group: int) -> None:
+    check(lib.mhd_group_synchronize(ctypes.c_void_p(group)), "mhd_group_synchronize")
+
+
+def mhd_group_destroy(group: int) -> None:
+    check(lib.mhd_group_destroy(ctypes.c_void_p(group)), "mhd_group_destroy")
 
 
 def mhd_mesh_query(mesh: int):

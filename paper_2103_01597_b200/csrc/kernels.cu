@@ -21,10 +21,9 @@ struct GAcc {
 };
 
 // MODE 0: RK3 update into `out` (which holds f_{k-1} for k > 0); MODE 1: RHS to rhs_out.
-// REMOTE: also deliver the new boundary values into the neighbours' halos (remote.cuh).
-template <typename T, int RAD, int MODE, bool REMOTE>
+template <typename T, int RAD, int MODE>
 __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out, Geom g, Region r, Coef<T> C,
-                                                     int k, T* __restrict__ rhs_out, RemoteMap<T> rm) {
+                                                     int k, T* __restrict__ rhs_out) {
   const int x = r.lo[0] + blockIdx.x * blockDim.x + threadIdx.x;
   const int y = r.lo[1] + blockIdx.y * blockDim.y + threadIdx.y;
   const int z = r.lo[2] + blockIdx.z * blockDim.z + threadIdx.z;
@@ -43,9 +42,15 @@ __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out
       fn[q] = rk_update<T>(k, D.f[q], fprev, rhs[q], C);
       out.f[q][base] = fn[q];
     }
-    if (REMOTE) {
-      remote_store<T, RAD>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, z, fn);
-      if (rm.sys) __threadfence_system();
+    if (g.xwrap) {
+      // periodic x faces (x unsplit), as in the z-marching kernel's epilogue: the cells of
+      // the first / last 32-byte sector of a row also go to the row padding on the other side
+      constexpr int W = 32 / (int)sizeof(T);
+      const long long sh = x < W ? (long long)g.nx : (x >= g.nx - W ? -(long long)g.nx : 0);
+      if (sh != 0) {
+#pragma unroll
+        for (int q = 0; q < NF; ++q) out.f[q][base + sh] = fn[q];
+      }
     }
   } else {
     const long long n = (long long)g.nx * g.ny * g.nz;
@@ -57,18 +62,15 @@ __global__ void __launch_bounds__(128) direct_kernel(Fields<T> in, Fields<T> out
 
 template <typename T, int RAD>
 void launch_direct(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, const RemoteMap<T>* rm) {
+                   const Coef<T>& C, int k, T* rhs_out) {
   if (r.ext[0] <= 0 || r.ext[1] <= 0 || r.ext[2] <= 0) return;
   // thin x-slabs of the outer shell get a block shaped along y
   const dim3 blk = r.ext[0] >= 16 ? dim3(32, 4, 1) : dim3(r.ext[0], (128 / r.ext[0]) < 32 ? (128 / r.ext[0]) : 32, 1);
   dim3 grd((r.ext[0] + blk.x - 1) / blk.x, (r.ext[1] + blk.y - 1) / blk.y, (r.ext[2] + blk.z - 1) / blk.z);
-  RemoteMap<T> none;
   if (rhs_out)
-    direct_kernel<T, RAD, 1, false><<<grd, blk, 0, st>>>(in, out, g, r, C, k, rhs_out, none);
-  else if (rm)
-    direct_kernel<T, RAD, 0, true><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr, *rm);
+    direct_kernel<T, RAD, 1><<<grd, blk, 0, st>>>(in, out, g, r, C, k, rhs_out);
   else
-    direct_kernel<T, RAD, 0, false><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr, none);
+    direct_kernel<T, RAD, 0><<<grd, blk, 0, st>>>(in, out, g, r, C, k, nullptr);
 }
 
 // ---- peer-memory exchange helpers -------------------------------------------------------------------
@@ -102,26 +104,39 @@ void launch_remote_copy(cudaStream_t st, const Fields<T>& fl, const Geom& g, con
   remote_copy_kernel<T><<<L.nblocks, 256, 0, st>>>(fl, g, L, rm);
 }
 
-// Cross-GPU ordering with system-scope flags.  Every operation that touches halos across ranks
-// (a boundary update that stores into the neighbours' halos, or a halo copy) has a sequence number
-// s and is bracketed by
+// Cross-GPU ordering with system-scope flags (process mode: one process per GPU).  Every operation
+// that touches halos across ranks (a boundary update whose results are copied into the neighbours'
+// halos, or a halo copy) has a sequence number s and is bracketed by
 //   sync(s):  publish arrive = s to every neighbour (all earlier work of this rank on the stream,
 //             reads of its own halo included, is complete), then wait until every neighbour has
 //             arrive >= s (it is done reading what we are about to overwrite) and done >= s - 1
 //             (its writes into our halo from the previous operation have landed);
 //   done(s):  after the remote stores, fence and publish done = s.
-__global__ void p2p_sync_kernel(FlagSet peer_arrive, FlagSet my_arrive, FlagSet my_done, unsigned long long seq) {
+// Ranks must enqueue their operations in lockstep (the same sequence on every rank).  A wait that
+// outlasts timeout_ns gives up and records s in *err (reported by the host) instead of trapping.
+__device__ __forceinline__ unsigned long long now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void p2p_sync_kernel(FlagSet peer_arrive, FlagSet my_arrive, FlagSet my_done, unsigned long long seq,
+                                unsigned long long* err, unsigned long long timeout_ns) {
   for (int i = 0; i < peer_arrive.n; ++i)
     asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(peer_arrive.ptr[i]), "l"(seq) : "memory");
+  const unsigned long long t0 = now_ns();
   for (int i = 0; i < my_arrive.n; ++i) {
-    const long long t0 = clock64();
-    for (;;) {
-      unsigned long long a, d;
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(a) : "l"(my_arrive.ptr[i]) : "memory");
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(d) : "l"(my_done.ptr[i]) : "memory");
-      if (a >= seq && d + 1 >= seq) break;
+    while (!(ld_acquire_sys(my_arrive.ptr[i]) >= seq && ld_acquire_sys(my_done.ptr[i]) + 1 >= seq)) {
       __nanosleep(128);
-      if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: a neighbour never arrived
+      if (now_ns() - t0 > timeout_ns) {
+        atomicMax(err, seq);
+        return;
+      }
     }
   }
 }
@@ -132,28 +147,54 @@ __global__ void p2p_signal_kernel(FlagSet fs, unsigned long long seq) {
     asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(fs.ptr[i]), "l"(seq) : "memory");
 }
 
-__global__ void p2p_wait_kernel(FlagSet fs, unsigned long long seq) {
+__global__ void p2p_wait_kernel(FlagSet fs, unsigned long long seq, unsigned long long* err,
+                                unsigned long long timeout_ns) {
+  const unsigned long long t0 = now_ns();
   for (int i = 0; i < fs.n; ++i) {
-    const long long t0 = clock64();
-    for (;;) {
-      unsigned long long v;
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(fs.ptr[i]) : "memory");
-      if (v >= seq) break;
+    while (ld_acquire_sys(fs.ptr[i]) < seq) {
       __nanosleep(128);
-      if (clock64() - t0 > 40000000000LL) __trap();
+      if (now_ns() - t0 > timeout_ns) {
+        atomicMax(err, seq);
+        return;
+      }
     }
   }
 }
 
 void launch_p2p_sync(cudaStream_t st, const FlagSet& peer_arrive, const FlagSet& my_arrive, const FlagSet& my_done,
-                     unsigned long long seq) {
-  p2p_sync_kernel<<<1, 1, 0, st>>>(peer_arrive, my_arrive, my_done, seq);
+                     unsigned long long seq, unsigned long long* err, unsigned long long timeout_ns) {
+  p2p_sync_kernel<<<1, 1, 0, st>>>(peer_arrive, my_arrive, my_done, seq, err, timeout_ns);
 }
 void launch_p2p_signal(cudaStream_t st, const FlagSet& fs, unsigned long long seq) {
   p2p_signal_kernel<<<1, 1, 0, st>>>(fs, seq);
 }
-void launch_p2p_wait(cudaStream_t st, const FlagSet& fs, unsigned long long seq) {
-  p2p_wait_kernel<<<1, 1, 0, st>>>(fs, seq);
+void launch_p2p_wait(cudaStream_t st, const FlagSet& fs, unsigned long long seq, unsigned long long* err,
+                     unsigned long long timeout_ns) {
+  p2p_wait_kernel<<<1, 1, 0, st>>>(fs, seq, err, timeout_ns);
+}
+
+// ---- debug: NaN poison of a state's halo ----------------------------------------------------------
+// Every cell of the halo-inclusive box [-r, n + r)^3 outside the interior, all 8 fields, gets a quiet
+// NaN: a stencil that reads a halo cell the schedule did not refresh (a corner that is not
+// exchanged; a z plane behind the TMA wrap; a stale face) turns the result into NaN.
+template <typename T>
+__global__ void __launch_bounds__(256) poison_kernel(Fields<T> F, Geom g, int rad) {
+  const int mx = g.nx + 2 * rad, my = g.ny + 2 * rad, mz = g.nz + 2 * rad;
+  const long long n = (long long)mx * my * mz;
+  const T nan = (T)__longlong_as_double(0x7ff8000000000000LL);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % mx) - rad;
+    const long long rr = i / mx;
+    const int y = (int)(rr % my) - rad, z = (int)(rr / my) - rad;
+    if (x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= 0 && z < g.nz) continue;
+    const long long o = (long long)z * g.sz + (long long)y * g.sy + x;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) F.f[q][o] = nan;
+  }
+}
+template <typename T>
+void launch_poison_halo(cudaStream_t st, const Fields<T>& fl, const Geom& g, int rad) {
+  poison_kernel<T><<<148 * 4, 256, 0, st>>>(fl, g, rad);
 }
 
 // ---- halo segments ---------------------------------------------------------
@@ -223,7 +264,9 @@ void launch_copy_out(cudaStream_t st, const TS* origin, TD* dst, const Geom& g) 
   copy_out_kernel<TS, TD><<<148 * 8, 256, 0, st>>>(origin, dst, g);
 }
 
-// ---- reductions (min, max, sum, sum of squares, sum of exp), two stages ----------------------------
+// ---- reductions (min, max, sum, and the sum of squares or of exp when asked), two stages --------------
+// min, max and sum are always formed (a NaN or Inf anywhere shows in the sum, so every reduction
+// checks finiteness); slot 3 holds the sum of squares (want == 3) or of exp (want == 4), else 0.
 __device__ __forceinline__ void red_combine(double* a, const double* b) {
   a[0] = fmin(a[0], b[0]);
   a[1] = fmax(a[1], b[1]);
@@ -233,7 +276,7 @@ __device__ __forceinline__ void red_combine(double* a, const double* b) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) reduce_stage1(const T* origin, Geom g, double* partial) {
+__global__ void __launch_bounds__(256) reduce_stage1(const T* origin, Geom g, double* partial, int want) {
   double v[kReduceVals] = {DBL_MAX, -DBL_MAX, 0.0, 0.0, 0.0};
   const long long n = (long long)g.nx * g.ny * g.nz;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -246,8 +289,8 @@ __global__ void __launch_bounds__(256) reduce_stage1(const T* origin, Geom g, do
     v[0] = fmin(v[0], f);
     v[1] = fmax(v[1], f);
     v[2] += f;
-    v[3] += f * f;
-    v[4] += exp(f);
+    if (want == 3) v[3] += f * f;
+    if (want == 4) v[4] += exp(f);
   }
   __shared__ double sh[256][kReduceVals];
   for (int j = 0; j < kReduceVals; ++j) sh[threadIdx.x][j] = v[j];
@@ -275,15 +318,15 @@ __global__ void reduce_stage2(double* partial, int nblocks) {
 }
 
 template <typename T>
-void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scratch, int nblocks) {
-  reduce_stage1<T><<<nblocks, 256, 0, st>>>(origin, g, scratch);
+void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scratch, int nblocks, int want) {
+  reduce_stage1<T><<<nblocks, 256, 0, st>>>(origin, g, scratch, want);
   reduce_stage2<<<1, 256, 0, st>>>(scratch, nblocks);
 }
 
 // ---- explicit instantiations ----------------------------------------------------------------------
 #define B2_DIRECT(T, RAD)                                                                               \
   template void launch_direct<T, RAD>(cudaStream_t, const Fields<T>&, const Fields<T>&, const Geom&,      \
-                                      const Region&, const Coef<T>&, int, T*, const RemoteMap<T>*);
+                                      const Region&, const Coef<T>&, int, T*);
 B2_DIRECT(float, 1)
 B2_DIRECT(float, 2)
 B2_DIRECT(float, 3)
@@ -297,7 +340,8 @@ B2_DIRECT(double, 4)
   template void launch_remote_copy<T>(cudaStream_t, const Fields<T>&, const Geom&, const SegList&,        \
                                       const RemoteMap<T>&);                                              \
   template void launch_segments<T>(cudaStream_t, const Fields<T>&, const Geom&, const SegList&, int, T*); \
-  template void launch_reduce<T>(cudaStream_t, const T*, const Geom&, double*, int);
+  template void launch_reduce<T>(cudaStream_t, const T*, const Geom&, double*, int, int);              \
+  template void launch_poison_halo<T>(cudaStream_t, const Fields<T>&, const Geom&, int);
 B2_INST(float)
 B2_INST(double)
 #undef B2_INST

@@ -24,7 +24,8 @@ struct Geom {
   long long sy, sz;
   int zwrap;  // z-marching kernel: fetch planes outside [0, nz) from their periodic image
               // instead of the z halo (one rank, z unsplit); 0: read the halo planes
-  int xwrap;  // z-marching kernel, plain variant: also store the periodic x faces of the output
+  int xwrap;  // update kernels: also store the periodic x faces of the output (x unsplit): the cells
+              // in the first / last 32-byte sector of a row go to the row padding on the other side
 };
 
 // One copy region of the halo machinery: cells of extent ext starting at src
@@ -51,7 +52,7 @@ struct Region {
 // ---- launchers (kernels.cu) ----
 template <typename T, int RAD>
 void launch_direct(cudaStream_t st, const Fields<T>& in, const Fields<T>& out, const Geom& g,
-                   const Region& r, const Coef<T>& C, int k, T* rhs_out, const RemoteMap<T>* rm = nullptr);
+                   const Region& r, const Coef<T>& C, int k, T* rhs_out);
 // peer-memory exchange: copy the remote segments of a state into the peers' halos; flags
 template <typename T>
 void launch_remote_copy(cudaStream_t st, const Fields<T>& fl, const Geom& g, const SegList& L, const RemoteMap<T>& rm);
@@ -59,10 +60,17 @@ struct FlagSet {
   unsigned long long* ptr[kMaxPeers];
   int n;
 };
+// Spin waits on flags written by other GPUs give up after `timeout_ns` (B2MHD_SPIN_TIMEOUT_S) and
+// record the sequence number they were waiting for in *err instead of trapping (a trap would
+// leave a sticky, unrecoverable context error); the host reports it (mhd_synchronize).
 void launch_p2p_signal(cudaStream_t st, const FlagSet& fs, unsigned long long seq);
 void launch_p2p_sync(cudaStream_t st, const FlagSet& peer_arrive, const FlagSet& my_arrive, const FlagSet& my_done,
-                     unsigned long long seq);
-void launch_p2p_wait(cudaStream_t st, const FlagSet& fs, unsigned long long seq);
+                     unsigned long long seq, unsigned long long* err, unsigned long long timeout_ns);
+void launch_p2p_wait(cudaStream_t st, const FlagSet& fs, unsigned long long seq, unsigned long long* err,
+                     unsigned long long timeout_ns);
+// debug (MHD_DEBUG_POISON_HALO): every halo cell of the 8 fields of a state <- quiet NaN
+template <typename T>
+void launch_poison_halo(cudaStream_t st, const Fields<T>& fl, const Geom& g, int rad);
 template <typename T>
 void launch_segments(cudaStream_t st, const Fields<T>& fl, const Geom& g, const SegList& L, int kind, T* buf);
 template <typename TS, typename TD>
@@ -70,7 +78,7 @@ void launch_copy_in(cudaStream_t st, const TS* src, TD* origin, const Geom& g);
 template <typename TS, typename TD>
 void launch_copy_out(cudaStream_t st, const TS* origin, TD* dst, const Geom& g);
 template <typename T>
-void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scratch, int nblocks);
+void launch_reduce(cudaStream_t st, const T* origin, const Geom& g, double* scratch, int nblocks, int want);
 
 // ---- z-marching TMA kernel (zmarch.cuh, one instantiation per dtype and radius) ----
 // TMA boxes per plane and field.  TMA requires the innermost start coordinate to be 16-byte
@@ -105,8 +113,7 @@ template <typename T, int RAD>
 bool zmarch_supported(const Geom& g, const Region& r);
 template <typename T, int RAD>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm = nullptr,
-                   bool persist = false, int zchunk = 0);
+                   const Coef<T>& C, int k, T* rhs_out, int xo, bool persist = false, int zchunk = 0);
 
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 constexpr int kReduceVals = 5;      // min, max, sum, sum of squares, sum of exp

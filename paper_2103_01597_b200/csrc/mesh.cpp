@@ -4,10 +4,13 @@
 //  * halo segments: 6 sides, 12 edges, 8 corners; segments to one peer are
 //    concatenated in canonical order, so one NCCL send/recv pair per distinct peer
 //    replaces the paper's per-segment MPI_Isend/Irecv with tags
-//  * the ISL iteration pipeline: pack on a high-priority comm stream, NCCL
-//    exchange there, the inner-segment update concurrently on the compute stream, then
-//    unpack -> event -> outer segments.  Stream order replaces the paper's per-iteration
+//  * the ISL iteration pipeline: pack on a high-priority comm stream, exchange
+//    there, the inner-segment update concurrently on the compute stream, then unpack -> outer
+//    segments -> event.  Stream order replaces the paper's per-iteration
 //    cudaDeviceSynchronize + MPI_Barrier.
+//  * ranks run either one per process (torchrun; cross-rank ordering by system-scope flags in
+//    peer memory) or several in one process (mhd_group_*: every rank's work is enqueued phase by
+//    phase and ordered by CUDA events, so no kernel ever waits for another).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -21,14 +24,12 @@
 #include <string>
 #include <vector>
 
-// How the periodic (self) halo of unsplit axes is kept, by schedule:
-//  * one rank: z planes through the TMA plane wrap (never stored), x faces by the plain z-march
-//    epilogue (Geom::xwrap), y rows by a copy launch;
-//  * several ranks (default, plain kernels): x faces by the plain epilogue, y rows copied;
-//  * several ranks with B2MHD_PLAIN=0: "wrap stores" of the storing (REMOTE) kernel variant,
-//    which writes every self segment (and the neighbours' halos) from its epilogue.
-// Measured history in DESIGN.md 2 and profiles/r01/ (bench_wab*, bench_xw2*, bench_pcopy*).
-// B2MHD_WRAP=0/1 forces the storing-variant wrap stores off/on (on one rank too).
+// How the periodic (self) halo of unsplit axes is kept:
+//  * one rank: z planes through the TMA plane wrap (never stored), x faces by the update
+//    kernels' epilogue (Geom::xwrap), y rows by a copy launch;
+//  * several ranks (z always split): x faces by the epilogue when x is unsplit, y rows copied.
+// (Round 1 also had a "storing" kernel variant that wrote every self and remote halo cell from
+// its epilogue; measured slower, it was removed: DESIGN.md 2, profiles/r01/bench_pcopy*.)
 
 #include "../../include/b2mhd.h"
 #include "kernels.h"
@@ -223,7 +224,7 @@ struct Layout {
   int64_t send_cells, recv_cells;
 };
 
-Layout make_layout(const mhd_mesh_info* info, int rank, const std::vector<SegInfo>& segs) {
+Layout make_layout(const mhd_mesh_info* info, const std::vector<SegInfo>& segs) {
   Layout L;
   int P[3];
   partition_xyz(info->nranks, P);
@@ -250,15 +251,16 @@ Layout make_layout(const mhd_mesh_info* info, int rank, const std::vector<SegInf
       L.send_cells += cells;
       L.recv_cells += cells;
     }
-  (void)rank;
   L.send_off = off;
   off = align_up(off + (size_t)L.send_cells * NF * es, 256);
   L.recv_off = off;
   off = align_up(off + (size_t)L.recv_cells * NF * es, 256);
   L.red_off = off;
   off = align_up(off + kReduceBlocks * kReduceVals * sizeof(double), 256);
-  L.flags_off = off;  // peer-memory exchange: arrive[nranks] then done[nranks], slot p written by rank p
-  off = align_up(off + 2 * (size_t)info->nranks * sizeof(unsigned long long), 256);
+  // peer-memory exchange flags: arrive[nranks] then done[nranks] (slot p written by rank p), then
+  // the spin-timeout word
+  L.flags_off = off;
+  off = align_up(off + (2 * (size_t)info->nranks + 1) * sizeof(unsigned long long), 256);
   L.total = off;
   return L;
 }
@@ -270,12 +272,21 @@ struct PeerXfer {
   int64_t send_cell0, send_cells, recv_cell0, recv_cells;
 };
 
+// Several ranks driven by one process (mhd_group_create): the meshes in rank order.
+struct mhd_group {
+  std::vector<mhd_mesh*> m;
+  int exchange = 0;
+};
+
+constexpr int kRing = 4;  // group mode: per-operation events, indexed by sequence number mod kRing
+
 struct mhd_mesh {
   mhd_mesh_info info;
   int P[3], coord[3];
   Layout L;
   Geom g;
   char* ws;
+  int device = 0;
   cudaStream_t stream;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
@@ -284,33 +295,21 @@ struct mhd_mesh {
   SegList self_list, pack_list, unpack_list;
   SegList self_list_xy;  // self segments without a z component (z halo fetched by TMA wrap)
   SegList self_list_y;   // ... and with a y component (x faces written by the update epilogue)
-  // Periodic x faces written by the plain z-march kernel's epilogue (Geom::xwrap: predicated
-  // stores of the cells within one sector of an x face; B2MHD_XWRAP=0 disables).  One rank:
-  // the y rows are then copied (0.014 ms instead of 0.06 ms for x and y) and the z planes are
-  // wrapped by TMA: 12.87 -> 13.1 Gcell/s FP64, 21.0 -> 22.2 FP32 (profiles/r01/bench_xw2_*).
-  // Several ranks with only x unsplit (4 GPUs): the inner segment uses it instead of the storing
-  // (REMOTE) variant.
+  SegList remote_list;   // remote segments, buf_off = peer slot (peer-memory exchange)
+  // Periodic x faces written by the update kernels' epilogue (Geom::xwrap: predicated stores of
+  // the cells within one sector of an x face; B2MHD_XWRAP=0 disables).  One rank: the y rows are
+  // then copied (0.014 ms instead of 0.06 ms for x and y) and the z planes are wrapped by TMA:
+  // 12.87 -> 13.1 Gcell/s FP64, 21.0 -> 22.2 FP32 (profiles/r01/bench_xw2_*).
   bool xwrap = true;
   bool x_valid = false;  // the x faces of the current state were written by the last update
   bool x_fits() const {
     const int64_t W = 32 / (int64_t)info.dtype;
     return xwrap && L.sy - L.xo - g.nx >= W && g.nx >= 2 * W;
   }
-  // the inner segment stores the periodic halo of unsplit axes itself (B2MHD_INNER_WRAP=0: give
-  // the unsplit axes boundary slabs instead, measured 25 % slower at 4 GPUs: the extra one-tile
-  // slab launches serialise on the side stream, profiles/r01/bench_iw*.json)
-  bool inner_wrap = true;
-  // Several ranks: plain z-march kernels everywhere, x faces by the plain epilogue, the remote
-  // halo by a copy kernel (p2p) or pack/unpack (NCCL), y rows copied when y is unsplit
-  // (B2MHD_PLAIN=0: the storing (REMOTE) variant instead).  Measured +6 % weak 4 GPUs, +5 % weak
-  // 2 GPUs, +2 % strong 4 GPUs for p2p (profiles/r01/bench_pcopy*.json).
-  bool plain = true;
-  bool plain_ok() const { return plain && x_fits() && variant != 1 && tmaps_ok; }
   // persistent z-march schedule (one CTA per SM slot, equal plane ranges; B2MHD_PERSIST=1, one
   // rank only): measured 8 % slower than the chunked grid (11.70 vs 12.66 Gcell/s,
-  // profiles/r01/bench_pers*.json) although it removes the wave tail and most chunk prologues:
-  // CTAs that run together no longer work on neighbouring tiles at the same z, so the halo
-  // rows they share stop hitting in L2.  Off by default.
+  // profiles/r01/bench_pers*.json): CTAs that run together no longer work on neighbouring tiles
+  // at the same z, so the halo rows they share stop hitting in L2.  Off by default.
   bool persist = false;
   int persist_env = -1;
   // z chunk of the boundary-slab launches on the side stream: 16 planes for FP32 (more, shorter
@@ -318,6 +317,7 @@ struct mhd_mesh {
   // 65.3 -> 82.7 Gcell/s at 4 GPUs), the default 64 for FP64 (16: -2 %; profiles/r01/bench_szc*).
   // B2MHD_SLAB_ZCHUNK=n overrides (0: 64).
   int slab_zchunk = -1;
+  int slab_env[3] = {0, 0, 0};
   ncclComm_t comm = nullptr;
   int cur = 0;
   int next_k = 0;
@@ -326,13 +326,21 @@ struct mhd_mesh {
   double* h_red = nullptr;  // pinned
   TmapSet tmaps[2];          // [state read with the stencil]
   bool tmaps_ok = false;
-  // peer-memory (NVLink) exchange
-  int exchange = 0;                 // 0: NCCL send/recv of packed segments; 1: fused peer-memory stores
+  // exchange of the remote halo: 0 = packed segments (NCCL send/recv between processes; a
+  // copy-engine pull from the neighbour's send buffer inside a group), 1 = peer memory (the new
+  // boundary cells stored straight into the neighbours' halos)
+  int exchange = 0;
+  mhd_group* group = nullptr;       // set: this rank is driven by mhd_group_* in this process
   std::vector<char*> peer_ws;       // workspace of every rank as mapped here (nullptr: not a neighbour)
   std::vector<void*> ipc_bases;     // opened IPC allocations (closed at destroy)
-  unsigned long long seq = 0;       // operations that touched halos across ranks
+  unsigned long long seq = 0;       // cross-rank operations so far (the same on every rank)
+  unsigned long long op_seq = 0;    // sequence number of the operation in progress
   bool halo_valid = false;          // halos of the current state already delivered by the last update
   bool self_valid = false;          // periodic self-wrap halo of the current state is up to date
+  FlagSet peer_arrive, peer_done, my_arrive, my_done;
+  unsigned long long spin_timeout_ns = 60ull * 1000000000ull;  // B2MHD_SPIN_TIMEOUT_S
+  cudaEvent_t ev_arrive[kRing] = {}, ev_done[kRing] = {};     // group mode
+  int debug = 0;                    // MHD_DEBUG_* flags
   // asynchronous host I/O (mhd_store_async / mhd_load_async): per direction a device staging
   // buffer (8 interior fields), a copy stream and per-field events: ev_dev = the device side of
   // the slot is done (gathered for a store, scattered into the state for a load), ev_host = the
@@ -343,40 +351,14 @@ struct mhd_mesh {
     cudaStream_t st = nullptr;
     cudaEvent_t ev_dev[NF] = {}, ev_host[NF] = {};
   } aio[2];  // [0] store (device -> host), [1] load (host -> device)
-  SegList remote_list;              // remote segments with buf_off = peer slot (halo copy after a load)
-  FlagSet peer_arrive, peer_done, my_arrive, my_done;
-  // The periodic self-wrap halo is written by the update kernels themselves: every cell
-  // within r of a face of an unsplit axis also stores its new value at its wrapped halo position
-  // (the same epilogue as the peer-memory send, with this rank's own state as the target), so the
-  // next substep needs no self-copy launch.  Slot `peers.size()` of the map is this rank.
-  bool wrap = false;
-  int slab_env[3] = {0, 0, 0};
-  bool wrap_stores() const { return wrap && self_list.n > 0 && peers.size() < (size_t)kMaxPeers; }
   template <typename T>
-  RemoteMap<T> remote_map(int dest_state, bool remote = true, bool self = false) const {
+  RemoteMap<T> remote_map(int dest_state) const {
     RemoteMap<T> rm;
     memset(&rm, 0, sizeof(rm));
-    for (int c = 0; c < 27; ++c) rm.peer_of[c] = -1;
-    rm.sys = remote && !peers.empty();
-    if (remote)
-      for (size_t i = 0; i < peers.size() && i < (size_t)kMaxPeers; ++i)
-        for (int q = 0; q < NF; ++q)
-          rm.f[i][q] = reinterpret_cast<T*>(peer_ws[peers[i].peer] + L.state_off[dest_state] +
-                                            (size_t)q * L.field_bytes) + L.origin;
-    const size_t me = peers.size();
-    if (self && wrap_stores())
+    for (size_t i = 0; i < peers.size() && i < (size_t)kMaxPeers; ++i)
       for (int q = 0; q < NF; ++q)
-        rm.f[me][q] = reinterpret_cast<T*>(ws + L.state_off[dest_state] + (size_t)q * L.field_bytes) + L.origin;
-    for (auto& si : segs) {
-      const int code = (si.s.offset[0] + 1) + 3 * (si.s.offset[1] + 1) + 9 * (si.s.offset[2] + 1);
-      if (si.self) {
-        if (self && wrap_stores()) rm.peer_of[code] = (signed char)me;
-        continue;
-      }
-      if (remote)
-        for (size_t i = 0; i < peers.size(); ++i)
-          if (peers[i].peer == si.s.send_peer) rm.peer_of[code] = (signed char)i;
-    }
+        rm.f[i][q] = reinterpret_cast<T*>(peer_ws[peers[i].peer] + L.state_off[dest_state] +
+                                          (size_t)q * L.field_bytes) + L.origin;
     return rm;
   }
   // profiling: (start, stop) event pairs per phase, with the algorithmic bytes of the launch
@@ -410,6 +392,8 @@ struct mhd_mesh {
   template <typename T>
   T* recv_buf() const { return reinterpret_cast<T*>(ws + L.recv_off); }
   double* red_scratch() const { return reinterpret_cast<double*>(ws + L.red_off); }
+  unsigned long long* flags() const { return reinterpret_cast<unsigned long long*>(ws + L.flags_off); }
+  unsigned long long* err_word() const { return flags() + 2 * info.nranks; }
   bool distributed() const { return info.nranks > 1; }
 };
 
@@ -459,8 +443,33 @@ SegList make_list(const mhd_mesh& m, bool self, bool send, bool no_z = false, bo
   return Ls;
 }
 
+// Remote segments for the peer-memory exchange: the P:705 send region of each segment, stored at
+// the receiver's halo position; buf_off = the peer's slot in the mesh's peer list.
+SegList make_remote_list(const mhd_mesh& m) {
+  SegList Ls;
+  memset(&Ls, 0, sizeof(Ls));
+  int nb = 0;
+  for (auto& si : m.segs) {
+    if (si.self) continue;
+    SegDesc& d = Ls.s[Ls.n++];
+    for (int a = 0; a < 3; ++a) {
+      d.src[a] = si.s.src_first[a];
+      d.dst[a] = si.s.dst_first[a];
+      d.ext[a] = si.s.extent[a];
+    }
+    d.count = (long long)d.ext[0] * d.ext[1] * d.ext[2];
+    d.buf_off = 0;
+    for (size_t i = 0; i < m.peers.size(); ++i)
+      if (m.peers[i].peer == si.s.send_peer) d.buf_off = (long long)i;
+    d.block0 = nb;
+    nb += (int)((d.count + 255) / 256);
+  }
+  Ls.nblocks = nb;
+  return Ls;
+}
+
 // TMA descriptors of the z-marching kernel: per state and field, a 3-D view
-// (x: row pitch sy, y: ny + 6 rows, z: nz + 6 planes) of the pitched field, with the halo box
+// (x: row pitch sy, y: ny + 2r rows, z: nz + 2r planes) of the pitched field, with the halo box
 // and the f_{k-1} box of the kernel's tile.
 mhd_status encode_tmaps(mhd_mesh* m) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -534,33 +543,78 @@ double seg_bytes(const SegList& L, size_t es) {
   return c * NF * (double)es * 2.0;
 }
 
+// ---- cross-rank ordering ---------------------------------------------------------------------------
+// Every operation that touches halos across ranks has a sequence number s (the same on every rank)
+// and two parts: a local part closed by xr_arrive(s), and a remote part opened by xr_wait(s).
+//  * Process mode (one process per GPU): xr_arrive is the flag kernel that publishes arrive = s to
+//    every neighbour and waits for each neighbour's arrive >= s and done >= s - 1 (kernels.cu);
+//    xr_wait is empty; xr_done publishes done = s.
+//  * Group mode (one process drives every rank, mhd_group_*): xr_arrive records an event; xr_wait
+//    makes the stream wait for every neighbour's arrive(s) and done(s - 1) events; xr_done records
+//    done(s).  The group driver runs a phase on every rank before the next phase on any, so each
+//    event is recorded before anyone waits on it, and no kernel ever waits for another (running
+//    waiting kernels of several ranks on one GPU can deadlock: B200_PROFILING.md).
+void xr_arrive(mhd_mesh* m, cudaStream_t st, unsigned long long s) {
+  if (m->group) {
+    cudaEventRecord(m->ev_arrive[s % kRing], st);
+  } else {
+    launch_p2p_sync(st, m->peer_arrive, m->my_arrive, m->my_done, s, m->err_word(), m->spin_timeout_ns);
+    m->launches++;
+  }
+}
+void xr_wait(mhd_mesh* m, cudaStream_t st, unsigned long long s) {
+  if (!m->group) return;  // the flag kernel of xr_arrive waited
+  for (auto& p : m->peers) {
+    mhd_mesh* n = m->group->m[p.peer];
+    cudaStreamWaitEvent(st, n->ev_arrive[s % kRing], 0);
+    if (s > 1) cudaStreamWaitEvent(st, n->ev_done[(s - 1) % kRing], 0);
+  }
+}
+void xr_done(mhd_mesh* m, cudaStream_t st, unsigned long long s) {
+  if (m->group) {
+    cudaEventRecord(m->ev_done[s % kRing], st);
+  } else {
+    launch_p2p_signal(st, m->peer_done, s);
+    m->launches++;
+  }
+}
+// wait until every neighbour finished operation s (its stores into this rank's halo have landed)
+void xr_wait_done(mhd_mesh* m, cudaStream_t st, unsigned long long s) {
+  if (s == 0 || m->peers.empty()) return;
+  if (m->group) {
+    for (auto& p : m->peers) cudaStreamWaitEvent(st, m->group->m[p.peer]->ev_done[s % kRing], 0);
+  } else {
+    launch_p2p_wait(st, m->my_done, s, m->err_word(), m->spin_timeout_ns);
+    m->launches++;
+  }
+}
+
 // The update of one region of the subdomain, with the kernels of the mesh's stencil radius.
 template <typename T, int RAD>
-void update_region_r(mhd_mesh* m, cudaStream_t st, const Region& r, int k, double dt, T* rhs_out,
-                     const RemoteMap<T>* rm) {
+void update_region_r(mhd_mesh* m, cudaStream_t st, const Region& r, int k, double dt, T* rhs_out) {
   const Fields<T> in = m->fields<T>(m->cur), out = m->fields<T>(1 - m->cur);
   const Coef<T> C = make_coef<T>(m->info, k, dt);
   const bool zm = m->variant != 1 && m->tmaps_ok && zmarch_supported<T, RAD>(m->g, r);
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
-  PhaseTimer t(m, st, st == m->stream ? MHD_PHASE_UPDATE : MHD_PHASE_OUTER, cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
+  PhaseTimer t(m, st, st == m->stream ? MHD_PHASE_UPDATE : MHD_PHASE_OUTER,
+               cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
   if (zm)
-    launch_zmarch<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, rm, m->persist,
+    launch_zmarch<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, m->persist,
                           st == m->stream ? 0 : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 0)));
   else
-    launch_direct<T, RAD>(st, in, out, m->g, r, C, k, rhs_out, rm);
+    launch_direct<T, RAD>(st, in, out, m->g, r, C, k, rhs_out);
   m->launches++;
 }
 
 template <typename T>
-void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out, const RemoteMap<T>* rm = nullptr,
-                   cudaStream_t st = nullptr) {
+void update_region(mhd_mesh* m, const Region& r, int k, double dt, T* rhs_out, cudaStream_t st = nullptr) {
   if (r.ext[0] <= 0 || r.ext[1] <= 0 || r.ext[2] <= 0) return;
   if (!st) st = m->stream;
   switch (m->info.radius) {
-    case 1: update_region_r<T, 1>(m, st, r, k, dt, rhs_out, rm); break;
-    case 2: update_region_r<T, 2>(m, st, r, k, dt, rhs_out, rm); break;
-    case 3: update_region_r<T, 3>(m, st, r, k, dt, rhs_out, rm); break;
-    case 4: update_region_r<T, 4>(m, st, r, k, dt, rhs_out, rm); break;
+    case 1: update_region_r<T, 1>(m, st, r, k, dt, rhs_out); break;
+    case 2: update_region_r<T, 2>(m, st, r, k, dt, rhs_out); break;
+    case 3: update_region_r<T, 3>(m, st, r, k, dt, rhs_out); break;
+    case 4: update_region_r<T, 4>(m, st, r, k, dt, rhs_out); break;
   }
 }
 
@@ -573,6 +627,16 @@ bool zmarch_ok(const mhd_mesh* m, const Region& r) {
     case 4: return zmarch_supported<T, 4>(m->g, r);
   }
   return false;
+}
+
+// MHD_DEBUG_POISON_HALO: before an update, NaN into every halo cell of the state it writes (its
+// interior holds f_{k-1}, read pointwise; its halo is refilled by this and the next substep's
+// exchange).  A cell the schedule fails to refresh before a stencil reads it poisons the result.
+template <typename T>
+void poison_out(mhd_mesh* m, T* rhs_out) {
+  if (!(m->debug & MHD_DEBUG_POISON_HALO) || rhs_out) return;
+  launch_poison_halo<T>(m->stream, m->fields<T>(1 - m->cur), m->g, m->info.radius);
+  m->launches++;
 }
 
 // Periodic self-copy of the halo, only when the last update did not already write it.
@@ -590,55 +654,15 @@ void ensure_self(mhd_mesh* m) {
   m->self_valid = true;
 }
 
-template <typename T>
-mhd_status halo_begin(mhd_mesh* m) {
-  const Fields<T> F = m->fields<T>(m->cur);
-  ensure_self<T>(m);
-  if (!m->distributed() || m->peers.empty()) return MHD_OK;
-  if (!m->comm) return fail(MHD_ENCCL, "mhd_comm_init was not called");
-  CU(cudaEventRecord(m->ev_ready, m->stream));
-  CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
-  {
-    PhaseTimer t(m, m->comm_stream, MHD_PHASE_PACK, seg_bytes(m->pack_list, sizeof(T)));
-    launch_segments<T>(m->comm_stream, F, m->g, m->pack_list, SEG_PACK, m->send_buf<T>());
-    m->launches++;
-  }
-  {
-    const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-    PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, seg_bytes(m->pack_list, sizeof(T)));
-    NC(ncclGroupStart());
-    for (auto& p : m->peers) {
-      NC(ncclSend(m->send_buf<T>() + p.send_cell0 * NF, (size_t)p.send_cells * NF, dt, p.peer, m->comm, m->comm_stream));
-      NC(ncclRecv(m->recv_buf<T>() + p.recv_cell0 * NF, (size_t)p.recv_cells * NF, dt, p.peer, m->comm, m->comm_stream));
-    }
-    NC(ncclGroupEnd());
-  }
-  {
-    PhaseTimer t(m, m->comm_stream, MHD_PHASE_UNPACK, seg_bytes(m->unpack_list, sizeof(T)));
-    launch_segments<T>(m->comm_stream, F, m->g, m->unpack_list, SEG_UNPACK, m->recv_buf<T>());
-    m->launches++;
-  }
-  CU(cudaEventRecord(m->ev_halo, m->comm_stream));
-  return MHD_OK;
-}
-
-template <typename T>
-mhd_status halo_end(mhd_mesh* m) {
-  if (m->distributed() && !m->peers.empty()) CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
-  return MHD_OK;
-}
-
 // Inner region and outer slabs: only axes split across ranks need the remote halo;
 // along unsplit axes the whole extent is inner (its halo is a self copy).  `thick` is the slab
-// width per axis: the radius r = 3 for the NCCL schedule, wider for the peer-memory schedule so
-// that the slabs run on the tiled kernel (a superset of the cells within r of a split boundary).
-void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer, const int thick_in[3],
-                   bool wrap_axes = false) {
+// width per axis (at least the radius; one tile wide so that the slabs run on the tiled kernel).
+void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer, const int thick_in[3]) {
   const int n[3] = {m->g.nx, m->g.ny, m->g.nz};
   bool split[3];
   int thick[3];
   for (int a = 0; a < 3; ++a) {
-    split[a] = m->P[a] > 1 || wrap_axes;
+    split[a] = m->P[a] > 1;
     thick[a] = std::max(m->info.radius, std::min(thick_in[a], n[a] / 2));
     inner.lo[a] = split[a] ? thick[a] : 0;
     inner.ext[a] = split[a] ? n[a] - 2 * thick[a] : n[a];
@@ -665,10 +689,10 @@ void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer,
 }
 
 // Boundary-slab widths (x, y, z): one tile wide in x and y so that the slabs run on the tiled
-// kernel; in z 8 planes for NCCL (the slabs wait for the exchange: keep them small) and 16 for
-// the peer-memory exchange (the slabs run first, beside the inner segment: fewer planes lost to
-// the 2r-plane prologue).  Measured at 256^3 per GPU (profiles/r01/bench_slab*.json): p2p 4 GPUs
-// 44.6 -> 45.9, 2 GPUs 22.7 -> 23.1 Gcell/s; NCCL best at 8.  B2MHD_SLAB="x,y,z" overrides.
+// kernel; in z 8 planes for the packed exchange (the slabs wait for it: keep them small) and 16
+// for the peer-memory exchange (the slabs run first, beside the inner segment: fewer planes lost
+// to the 2r-plane prologue).  Measured at 256^3 per GPU (profiles/r01/bench_slab*.json): p2p 4
+// GPUs 44.6 -> 45.9, 2 GPUs 22.7 -> 23.1 Gcell/s; NCCL best at 8.  B2MHD_SLAB="x,y,z" overrides.
 template <typename T>
 void slab_thickness(const mhd_mesh* m, int thick[3]) {
   thick[0] = zm_tx<T>();
@@ -680,57 +704,72 @@ void slab_thickness(const mhd_mesh* m, int thick[3]) {
     for (int a = 0; a < 3; ++a) thick[a] = m->slab_env[a];
 }
 
-// Peer-memory exchange.  Per substep: wait until every neighbour finished its
-// previous cross-rank operation; update the outer shell, storing boundary results locally and into
-// the neighbours' halos; publish; then update the inner segment (which needs no remote halo) while
-// the neighbours proceed.
+// ---- the operations of the schedules, phase by phase ----------------------------------------------
+// Each returns MHD_OK; phase 0 is the local part (ends with xr_arrive where there is a cross-rank
+// step), phase 1 the remote part.  Process mode runs both phases of one mesh back to back; a
+// group runs phase 0 of every rank, then phase 1 of every rank (run_phases).
+
+// Peer-memory halo copy of the current state (after a load, or for mhd_halo_exchange): the P:705
+// send regions straight into the neighbours' halos.
 template <typename T>
-void p2p_halo_copy(mhd_mesh* m) {
-  const unsigned long long s = ++m->seq;
-  launch_p2p_sync(m->stream, m->peer_arrive, m->my_arrive, m->my_done, s);
-  const RemoteMap<T> rm = m->remote_map<T>(m->cur);
-  launch_remote_copy<T>(m->stream, m->fields<T>(m->cur), m->g, m->remote_list, rm);
-  launch_p2p_signal(m->stream, m->peer_done, s);
-  m->launches += 3;
-  m->halo_valid = true;
+mhd_status op_p2p_halo_copy(mhd_mesh* m, int ph) {
+  if (ph == 0) {
+    ensure_self<T>(m);
+    m->op_seq = ++m->seq;
+    xr_arrive(m, m->stream, m->op_seq);
+  } else {
+    const unsigned long long s = m->op_seq;
+    xr_wait(m, m->stream, s);
+    {
+      PhaseTimer t(m, m->stream, MHD_PHASE_PACK, seg_bytes(m->remote_list, sizeof(T)));
+      launch_remote_copy<T>(m->stream, m->fields<T>(m->cur), m->g, m->remote_list, m->remote_map<T>(m->cur));
+      m->launches++;
+    }
+    xr_done(m, m->stream, s);
+    m->halo_valid = true;
+  }
+  CU(cudaGetLastError());
+  return MHD_OK;
 }
 
-// Peer-memory exchange with the plain kernel everywhere (the default; B2MHD_PLAIN=0 selects the
-// storing variant below): the boundary slabs
-// and the inner segment run the plain z-march (x faces by its predicated epilogue stores when x
-// is unsplit), and one copy kernel on the side stream then pushes the new boundary cells into
-// the neighbours' halos (the segments of P:705, all in the just-written slabs), before the
-// completion flag.  The y halo of an unsplit y axis is copied at the next substep's start.
+// Peer-memory substep.  Side stream (high priority): wait until every
+// neighbour is done with its previous operation, update the boundary slabs (one tile thick), then
+// one copy kernel stores the new boundary cells (the send regions of P:705, all inside the slabs
+// just written, L2-hot) into the neighbours' halos of the new state, and publishes done.  Compute
+// stream, concurrently: the inner segment (needs no remote halo).  The x faces of an unsplit x
+// axis are written by every update's epilogue; the y halo of an unsplit y axis is copied at the
+// next substep's start.
 template <typename T>
-mhd_status substep_p2p_copy(mhd_mesh* m, int k, double dt, T* rhs_out) {
-  const bool xw = m->P[0] == 1;
-  ensure_self<T>(m);
-  if (!m->halo_valid) p2p_halo_copy<T>(m);
+mhd_status op_p2p_substep(mhd_mesh* m, int ph, int k, double dt, T* rhs_out) {
+  const bool xw = m->P[0] == 1 && m->x_fits();
+  if (ph == 0) {
+    poison_out<T>(m, rhs_out);
+    ensure_self<T>(m);
+    m->op_seq = ++m->seq;
+    CU(cudaEventRecord(m->ev_ready, m->stream));
+    CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
+    PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, 0.0);
+    xr_arrive(m, m->comm_stream, m->op_seq);
+    CU(cudaGetLastError());
+    return MHD_OK;
+  }
+  const unsigned long long s = m->op_seq;
   Region inner;
   std::vector<Region> outer;
   int thick[3];
   slab_thickness<T>(m, thick);
   split_regions(m, inner, outer, thick);
-  const unsigned long long s = ++m->seq;
-  CU(cudaEventRecord(m->ev_ready, m->stream));
-  CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
-  {
-    PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, 0.0);
-    launch_p2p_sync(m->comm_stream, m->peer_arrive, m->my_arrive, m->my_done, s);
-    m->launches++;
-  }
+  xr_wait(m, m->comm_stream, s);
   m->g.xwrap = !rhs_out && xw ? 1 : 0;
-  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, nullptr, m->comm_stream);
+  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, m->comm_stream);
   if (!rhs_out) {
-    const RemoteMap<T> rm = m->remote_map<T>(1 - m->cur);
     PhaseTimer t(m, m->comm_stream, MHD_PHASE_PACK, seg_bytes(m->remote_list, sizeof(T)));
-    launch_remote_copy<T>(m->comm_stream, m->fields<T>(1 - m->cur), m->g, m->remote_list, rm);
+    launch_remote_copy<T>(m->comm_stream, m->fields<T>(1 - m->cur), m->g, m->remote_list, m->remote_map<T>(1 - m->cur));
     m->launches++;
   }
-  launch_p2p_signal(m->comm_stream, m->peer_done, s);
-  m->launches++;
+  xr_done(m, m->comm_stream, s);
   CU(cudaEventRecord(m->ev_halo, m->comm_stream));
-  update_region<T>(m, inner, k, dt, rhs_out, nullptr);
+  update_region<T>(m, inner, k, dt, rhs_out);
   m->g.xwrap = 0;
   CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
   if (!rhs_out) {
@@ -742,46 +781,97 @@ mhd_status substep_p2p_copy(mhd_mesh* m, int k, double dt, T* rhs_out) {
   return MHD_OK;
 }
 
+// Packed exchange of the current state's remote halo on the side stream: pack ->
+// transfer -> unpack.  Transfer: NCCL grouped send/recv per distinct peer between processes; in a
+// group, each rank pulls its neighbours' send-buffer slices into its receive buffer with the copy
+// engines (cudaMemcpyAsync over NVLink or within a device), ordered by events.
+// Phase 0 ends after the pack (group) or the unpack (NCCL); phase 1 completes the transfer.
 template <typename T>
-mhd_status substep_p2p(mhd_mesh* m, int k, double dt, T* rhs_out) {
-  if (m->plain_ok()) return substep_p2p_copy<T>(m, k, dt, rhs_out);
-  ensure_self<T>(m);
-  if (!m->halo_valid) p2p_halo_copy<T>(m);
+mhd_status xchg_packed(mhd_mesh* m, int ph) {
+  const Fields<T> F = m->fields<T>(m->cur);
+  if (ph == 0) {
+    ensure_self<T>(m);
+    CU(cudaEventRecord(m->ev_ready, m->stream));
+    CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
+    if (m->group) {
+      m->op_seq = ++m->seq;
+      xr_wait_done(m, m->comm_stream, m->op_seq - 1);  // neighbours finished pulling the last pack
+    } else if (!m->comm) {
+      return fail(MHD_ENCCL, "mhd_comm_init was not called");
+    }
+    {
+      PhaseTimer t(m, m->comm_stream, MHD_PHASE_PACK, seg_bytes(m->pack_list, sizeof(T)));
+      launch_segments<T>(m->comm_stream, F, m->g, m->pack_list, SEG_PACK, m->send_buf<T>());
+      m->launches++;
+    }
+    if (m->group) {
+      xr_arrive(m, m->comm_stream, m->op_seq);
+      CU(cudaGetLastError());
+      return MHD_OK;
+    }
+    {
+      const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+      PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, seg_bytes(m->pack_list, sizeof(T)));
+      NC(ncclGroupStart());
+      for (auto& p : m->peers) {
+        NC(ncclSend(m->send_buf<T>() + p.send_cell0 * NF, (size_t)p.send_cells * NF, dt, p.peer, m->comm, m->comm_stream));
+        NC(ncclRecv(m->recv_buf<T>() + p.recv_cell0 * NF, (size_t)p.recv_cells * NF, dt, p.peer, m->comm, m->comm_stream));
+      }
+      NC(ncclGroupEnd());
+    }
+  } else {
+    if (!m->group) return MHD_OK;
+    const unsigned long long s = m->op_seq;
+    xr_wait(m, m->comm_stream, s);
+    {
+      PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, seg_bytes(m->pack_list, sizeof(T)));
+      for (auto& p : m->peers) {
+        const mhd_mesh* n = m->group->m[p.peer];
+        for (auto& q : n->peers)
+          if (q.peer == m->info.rank) {
+            if (q.send_cells != p.recv_cells) return fail(MHD_EINVAL, "group: peer buffer sizes disagree");
+            CU(cudaMemcpyAsync(m->recv_buf<T>() + p.recv_cell0 * NF, n->send_buf<T>() + q.send_cell0 * NF,
+                               (size_t)p.recv_cells * NF * sizeof(T), cudaMemcpyDefault, m->comm_stream));
+          }
+      }
+    }
+    xr_done(m, m->comm_stream, s);
+  }
+  if (ph == (m->group ? 1 : 0)) {
+    PhaseTimer t(m, m->comm_stream, MHD_PHASE_UNPACK, seg_bytes(m->unpack_list, sizeof(T)));
+    launch_segments<T>(m->comm_stream, F, m->g, m->unpack_list, SEG_UNPACK, m->recv_buf<T>());
+    m->launches++;
+  }
+  CU(cudaGetLastError());
+  return MHD_OK;
+}
+
+// Substep with the packed exchange (the paper's scheme): the exchange on the side
+// stream, then the boundary slabs there; the inner segment concurrently on the compute stream.
+template <typename T>
+mhd_status op_packed_substep(mhd_mesh* m, int ph, int k, double dt, T* rhs_out) {
+  if (m->peers.empty()) return fail(MHD_EINVAL, "distributed mesh without peers");
+  if (ph == 0) {
+    poison_out<T>(m, rhs_out);
+    return xchg_packed<T>(m, 0);
+  }
+  mhd_status st = xchg_packed<T>(m, 1);
+  if (st != MHD_OK) return st;
+  const bool xw = m->P[0] == 1 && m->x_fits();
   Region inner;
   std::vector<Region> outer;
   int thick[3];
   slab_thickness<T>(m, thick);
-  // optionally (B2MHD_INNER_WRAP=0) the unsplit axes get boundary slabs too, so that the inner
-  // segment runs the plain kernel
-  const bool wsplit = m->wrap_stores() && !m->inner_wrap;
-  split_regions(m, inner, outer, thick, wsplit);
-  const unsigned long long s = ++m->seq;
-  // high-priority side stream: sync, boundary slabs (update + store into the neighbours' halos,
-  // the fused send), publish; the inner segment needs no remote halo and runs concurrently on the
-  // compute stream, filling the SMs the thin slab launches leave idle
-  CU(cudaEventRecord(m->ev_ready, m->stream));
-  CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
-  {
-    PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, 0.0);
-    launch_p2p_sync(m->comm_stream, m->peer_arrive, m->my_arrive, m->my_done, s);
-    m->launches++;
-  }
-  const RemoteMap<T> rm = m->remote_map<T>(1 - m->cur, true, true);
-  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, rhs_out ? nullptr : &rm, m->comm_stream);
-  launch_p2p_signal(m->comm_stream, m->peer_done, s);
-  m->launches++;
+  split_regions(m, inner, outer, thick);
+  m->g.xwrap = !rhs_out && xw ? 1 : 0;
+  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, m->comm_stream);
   CU(cudaEventRecord(m->ev_halo, m->comm_stream));
-  // inner segment: the periodic halo of the unsplit axes through the storing variant, the same
-  // kernel binary as the concurrent boundary slabs (the plain kernel with its x-face stores,
-  // the 1-GPU choice, ran 12 % slower here: two different z-march binaries side by side,
-  // profiles/r01/bench_x2_weak4_*.json)
-  const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
-  const bool inner_wrap = !rhs_out && m->wrap_stores() && !wsplit;
-  update_region<T>(m, inner, k, dt, rhs_out, inner_wrap ? &wm : nullptr);
+  update_region<T>(m, inner, k, dt, rhs_out);
   CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
+  m->g.xwrap = 0;
   if (!rhs_out) {
-    m->halo_valid = true;  // the neighbours are delivering the new state's halo
-    m->self_valid = m->wrap_stores();
+    m->self_valid = !m->self_list.n || (xw && !m->self_list_y.n);
+    m->x_valid = xw;
   }
   CU(cudaGetLastError());
   return MHD_OK;
@@ -800,6 +890,7 @@ mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
   const bool zm = m->variant != 1 && m->tmaps_ok && zmarch_ok<T>(m, full);
   const bool zw = !m->self_valid && zm;
   const bool xw = zw && m->x_valid;
+  poison_out<T>(m, rhs_out);
   if (!m->self_valid && m->self_list.n) {
     const SegList& L = xw ? m->self_list_y : (zw ? m->self_list_xy : m->self_list);
     PhaseTimer t(m, m->stream, MHD_PHASE_SELF, seg_bytes(L, sizeof(T)));
@@ -807,62 +898,95 @@ mhd_status substep_local(mhd_mesh* m, int k, double dt, T* rhs_out) {
     m->launches++;
   }
   m->self_valid = !zw;  // the z halo of the current state stays stale with the TMA wrap
-  const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
-  const bool use_x = !rhs_out && !m->wrap_stores() && zw && m->x_fits();
+  const bool use_x = !rhs_out && zw && m->x_fits();
   m->g.zwrap = zw ? 1 : 0;
   m->g.xwrap = use_x ? 1 : 0;
   m->persist = m->persist_env == 1;
-  update_region<T>(m, full, k, dt, rhs_out, rhs_out || !m->wrap_stores() ? nullptr : &wm);
+  update_region<T>(m, full, k, dt, rhs_out);
   m->persist = false;
   m->g.zwrap = 0;
   m->g.xwrap = 0;
   if (!rhs_out) {
-    m->self_valid = m->wrap_stores();
+    m->self_valid = false;
     m->x_valid = use_x;
   }
   CU(cudaGetLastError());
   return MHD_OK;
 }
 
-template <typename T>
-mhd_status substep_impl(mhd_mesh* m, int k, double dt, T* rhs_out) {
-  if (m->exchange == 1) return substep_p2p<T>(m, k, dt, rhs_out);
-  if (!m->distributed()) return substep_local<T>(m, k, dt, rhs_out);
-  mhd_status st = halo_begin<T>(m);
-  if (st != MHD_OK) return st;
-  Region inner;
-  std::vector<Region> outer;
-  // slabs one tile thick so that they run on the tiled kernel; they follow the unpack on the
-  // high-priority comm stream, concurrently with the inner segment on the compute stream
-  int thick[3];
-  slab_thickness<T>(m, thick);
-  const bool plain = m->plain_ok();  // plain kernels, x faces by their epilogue (see substep_p2p_copy)
-  const bool xw = plain && m->P[0] == 1;
-  const bool wsplit = !plain && m->wrap_stores() && !m->inner_wrap;  // as in substep_p2p
-  split_regions(m, inner, outer, thick, wsplit);
-  const RemoteMap<T> wm = m->remote_map<T>(1 - m->cur, false, true);
-  const RemoteMap<T>* w = rhs_out || plain || !m->wrap_stores() ? nullptr : &wm;
-  const RemoteMap<T>* wi = wsplit ? nullptr : w;  // same binary as the slabs (see substep_p2p)
-  m->g.xwrap = !rhs_out && xw ? 1 : 0;
-  if (m->peers.empty()) {
-    update_region<T>(m, inner, k, dt, rhs_out, wi);
-    for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, w);
-  } else {
-    for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, w, m->comm_stream);
-    CU(cudaEventRecord(m->ev_halo, m->comm_stream));
-    update_region<T>(m, inner, k, dt, rhs_out, wi);
-    CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
-  }
-  m->g.xwrap = 0;
-  if (!rhs_out) {
-    if (plain) {
-      m->self_valid = !m->self_list.n || (xw && !m->self_list_y.n);
-      m->x_valid = xw;
-    } else {
-      m->self_valid = m->wrap_stores();
+// Runs an operation of `nph` phases over the meshes of one process: phase p of every mesh before
+// phase p + 1 of any (a single mesh: its phases back to back).  Each mesh's device is made current
+// while its work is enqueued; the caller's current device is restored.
+template <class F>
+mhd_status run_phases(mhd_mesh* const* ms, int n, int nph, F&& f) {
+  int dev0 = -1;
+  if (n > 1) CU(cudaGetDevice(&dev0));
+  mhd_status st = MHD_OK;
+  for (int ph = 0; ph < nph && st == MHD_OK; ++ph)
+    for (int i = 0; i < n && st == MHD_OK; ++i) {
+      if (n > 1) CU(cudaSetDevice(ms[i]->device));
+      st = f(ms[i], i, ph);
     }
+  if (dev0 >= 0) CU(cudaSetDevice(dev0));
+  return st;
+}
+
+// One substep of every mesh of `ms` (one process-mode mesh, or every rank of a group).
+template <typename T>
+mhd_status substep_all(mhd_mesh* const* ms, int n, int k, double dt, T* const* rhs) {
+  mhd_mesh* m0 = ms[0];
+  if (!m0->distributed()) return substep_local<T>(m0, k, dt, rhs ? rhs[0] : nullptr);
+  auto R = [&](int i) { return rhs ? rhs[i] : nullptr; };
+  if (m0->exchange == 1) {
+    if (!m0->halo_valid) {
+      mhd_status st = run_phases(ms, n, 2, [&](mhd_mesh* m, int, int ph) { return op_p2p_halo_copy<T>(m, ph); });
+      if (st != MHD_OK) return st;
+    }
+    return run_phases(ms, n, 2, [&](mhd_mesh* m, int i, int ph) { return op_p2p_substep<T>(m, ph, k, dt, R(i)); });
   }
-  CU(cudaGetLastError());
+  return run_phases(ms, n, 2, [&](mhd_mesh* m, int i, int ph) { return op_packed_substep<T>(m, ph, k, dt, R(i)); });
+}
+
+// Fill the halo of the current state of every mesh of `ms`.
+template <typename T>
+mhd_status halo_exchange_all(mhd_mesh* const* ms, int n) {
+  mhd_mesh* m0 = ms[0];
+  if (!m0->distributed()) {
+    ensure_self<T>(m0);
+    CU(cudaGetLastError());
+    return MHD_OK;
+  }
+  if (m0->exchange == 1)
+    return run_phases(ms, n, 3, [&](mhd_mesh* m, int, int ph) -> mhd_status {
+      if (ph < 2) return op_p2p_halo_copy<T>(m, ph);
+      xr_wait_done(m, m->stream, m->seq);  // the neighbours' copies into this halo have landed
+      CU(cudaGetLastError());
+      return MHD_OK;
+    });
+  return run_phases(ms, n, 2, [&](mhd_mesh* m, int, int ph) -> mhd_status {
+    if (m->peers.empty()) return ph == 0 ? (ensure_self<T>(m), MHD_OK) : MHD_OK;
+    mhd_status st = xchg_packed<T>(m, ph);
+    if (st != MHD_OK || ph == 0) return st;
+    CU(cudaEventRecord(m->ev_halo, m->comm_stream));
+    CU(cudaStreamWaitEvent(m->stream, m->ev_halo, 0));
+    return MHD_OK;
+  });
+}
+
+// Peer-memory exchange, process mode: before the host reuses or releases memory that neighbours
+// may still be storing into, wait for their last operation to land.
+void settle_remote(mhd_mesh* m) {
+  if (m->exchange == 1 && m->distributed() && m->seq > 0) xr_wait_done(m, m->stream, m->seq);
+}
+
+// Spin waits that timed out (process-mode peer-memory exchange) leave the sequence number in the
+// error word; a blocking call reports it.
+mhd_status check_spin(mhd_mesh* m) {
+  if (!(m->exchange == 1 && m->distributed() && !m->group)) return MHD_OK;
+  unsigned long long e = 0;
+  CU(cudaMemcpy(&e, m->err_word(), sizeof(e), cudaMemcpyDeviceToHost));
+  if (e) return fail(MHD_ECUDA, "peer-memory exchange: a neighbour did not arrive at operation " + std::to_string(e) +
+                                    " within B2MHD_SPIN_TIMEOUT_S (ranks must run the same substeps in lockstep)");
   return MHD_OK;
 }
 
@@ -874,6 +998,13 @@ mhd_status load_impl(mhd_mesh* m, int field, const void* src, int src_dtype, int
   TM* origin = m->fields<TM>(m->cur).f[field];
   const size_t es = (size_t)src_dtype;
   const size_t ncell = (size_t)m->g.nx * m->g.ny * m->g.nz;
+  settle_remote(m);
+  if (m->debug & MHD_DEBUG_POISON_HALO) {
+    Fields<TM> one = m->fields<TM>(m->cur);
+    for (int q = 0; q < NF; ++q) one.f[q] = one.f[field];
+    launch_poison_halo<TM>(m->stream, one, m->g, m->info.radius);
+    m->launches++;
+  }
   if (src_dtype == (int)sizeof(TM)) {
     cudaMemcpy3DParms p;
     memset(&p, 0, sizeof(p));
@@ -931,9 +1062,67 @@ mhd_status store_impl(mhd_mesh* m, int field, void* dst, int dst_dtype, int on_d
       CU(cudaFreeAsync(tmp, m->stream));
     }
   }
-  if (!on_device) CU(cudaStreamSynchronize(m->stream));
+  if (!on_device) {
+    CU(cudaStreamSynchronize(m->stream));
+    return check_spin(m);
+  }
   return MHD_OK;
 }
+
+// Local partial reduction of one field of the current state into v[kReduceVals] on the host
+// (min, max, sum, sum of squares, sum of exp; slots 3/4 only when asked).
+mhd_status reduce_local(mhd_mesh* m, int field, int op, bool finish_on_host) {
+  double* sc = m->red_scratch();
+  const int want = op == MHD_RMS ? 3 : (op == MHD_SUM_EXP ? 4 : 0);
+  if (m->info.dtype == MHD_F64)
+    launch_reduce<double>(m->stream, m->fields<double>(m->cur).f[field], m->g, sc, kReduceBlocks, want);
+  else
+    launch_reduce<float>(m->stream, m->fields<float>(m->cur).f[field], m->g, sc, kReduceBlocks, want);
+  m->launches += 2;
+  if (finish_on_host) CU(cudaMemcpyAsync(m->h_red, sc, kReduceVals * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaGetLastError());
+  return MHD_OK;
+}
+
+mhd_status reduce_finish(const double* v, const mhd_mesh_info& info, int op, double* out) {
+  const double ncell = (double)info.n[0] * (double)info.n[1] * (double)info.n[2];
+  double r = 0;
+  switch (op) {
+    case MHD_MIN: r = v[0]; break;
+    case MHD_MAX: r = v[1]; break;
+    case MHD_SUM: r = v[2]; break;
+    case MHD_RMS: r = std::sqrt(v[3] / ncell); break;
+    case MHD_SUM_EXP: r = v[4]; break;
+  }
+  *out = r;
+  if (!std::isfinite(v[0]) || !std::isfinite(v[1]) || !std::isfinite(v[2]) || !std::isfinite(r))
+    return fail(MHD_ENONFINITE, "field holds a NaN or Inf (or the statistic overflows)");
+  return MHD_OK;
+}
+
+mhd_status open_peers(mhd_mesh* m) {
+  m->remote_list = make_remote_list(*m);
+  memset(&m->peer_arrive, 0, sizeof(FlagSet));
+  memset(&m->peer_done, 0, sizeof(FlagSet));
+  memset(&m->my_arrive, 0, sizeof(FlagSet));
+  memset(&m->my_done, 0, sizeof(FlagSet));
+  const int nr = m->info.nranks;
+  for (auto& p : m->peers) {
+    if (!m->peer_ws[p.peer]) return fail(MHD_EINVAL, "neighbour workspace not mapped");
+    unsigned long long* peer_flags = reinterpret_cast<unsigned long long*>(m->peer_ws[p.peer] + m->L.flags_off);
+    unsigned long long* my_flags = m->flags();
+    m->peer_arrive.ptr[m->peer_arrive.n++] = peer_flags + m->info.rank;
+    m->peer_done.ptr[m->peer_done.n++] = peer_flags + nr + m->info.rank;
+    m->my_arrive.ptr[m->my_arrive.n++] = my_flags + p.peer;
+    m->my_done.ptr[m->my_done.n++] = my_flags + nr + p.peer;
+  }
+  m->halo_valid = false;
+  m->self_valid = false;
+  m->x_valid = false;
+  return MHD_OK;
+}
+
+bool in_group(const mhd_mesh* m) { return m->group != nullptr; }
 }  // namespace
 
 // =================================================================================================
@@ -996,7 +1185,7 @@ mhd_status mhd_workspace_bytes(const mhd_mesh_info* info, size_t* bytes) {
   if (st != MHD_OK) return st;
   if (!bytes) return fail(MHD_EINVAL, "bytes is null");
   auto segs = build_segments(info, info->rank);
-  *bytes = make_layout(info, info->rank, segs).total;
+  *bytes = make_layout(info, segs).total;
   return MHD_OK;
 }
 
@@ -1007,18 +1196,16 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   if (!dev_workspace || !out) return fail(MHD_EINVAL, "null workspace or out");
   mhd_mesh* m = new mhd_mesh();
   m->info = *info;
-  m->wrap = info->nranks > 1;
-  if (const char* w = getenv("B2MHD_WRAP")) m->wrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_XWRAP")) m->xwrap = atoi(w) != 0;
-  if (const char* w = getenv("B2MHD_INNER_WRAP")) m->inner_wrap = atoi(w) != 0;
-  if (const char* w = getenv("B2MHD_PLAIN")) m->plain = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_PERSIST")) m->persist_env = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_SLAB_ZCHUNK")) m->slab_zchunk = atoi(w);
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
+  if (const char* w = getenv("B2MHD_POISON")) m->debug |= atoi(w) ? MHD_DEBUG_POISON_HALO : 0;
+  if (const char* w = getenv("B2MHD_SPIN_TIMEOUT_S")) m->spin_timeout_ns = (unsigned long long)(atof(w) * 1e9);
   partition_xyz(info->nranks, m->P);
   coord_xyz(info->rank, m->coord);
   m->segs = build_segments(info, info->rank);
-  m->L = make_layout(info, info->rank, m->segs);
+  m->L = make_layout(info, m->segs);
   if (bytes < m->L.total) {
     delete m;
     return fail(MHD_ENOMEM, "workspace smaller than mhd_workspace_bytes");
@@ -1032,6 +1219,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->g.xwrap = 0;
   m->ws = static_cast<char*>(dev_workspace);
   m->stream = static_cast<cudaStream_t>(cuda_stream);
+  cudaGetDevice(&m->device);
   // peers in rank order, each with a contiguous slice of the send and recv buffers
   std::vector<int64_t> scount(info->nranks, 0), rcount(info->nranks, 0);
   for (auto& si : m->segs)
@@ -1053,7 +1241,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->pack_list = make_list(*m, false, true);
   m->unpack_list = make_list(*m, false, false);
   cudaError_t e = cudaMemsetAsync(m->ws, 0, m->L.total, m->stream);
-  if (e == cudaSuccess) {  // side stream: halo exchange (N > 1) or the periodic self-copy (N = 1)
+  if (e == cudaSuccess) {  // side stream: halo exchange and the boundary slabs (N > 1)
     int lo, hi;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     e = cudaStreamCreateWithPriority(&m->comm_stream, cudaStreamNonBlocking, hi);
@@ -1085,6 +1273,7 @@ mhd_status mhd_nccl_unique_id(void* out128) {
 mhd_status mhd_comm_init(mhd_mesh* m, const void* nccl_unique_id) {
   if (!m || !nccl_unique_id) return fail(MHD_EINVAL, "null argument");
   if (m->info.nranks == 1) return MHD_OK;
+  if (in_group(m)) return fail(MHD_EINVAL, "mesh belongs to a group (no NCCL communicator)");
   ncclUniqueId id;
   memcpy(&id, nccl_unique_id, sizeof(id));
   NC(ncclCommInitRank(&m->comm, m->info.nranks, id, m->info.rank));
@@ -1093,12 +1282,20 @@ mhd_status mhd_comm_init(mhd_mesh* m, const void* nccl_unique_id) {
 
 mhd_status mhd_mesh_destroy(mhd_mesh* m) {
   if (!m) return MHD_OK;
+  if (m->group) return fail(MHD_EINVAL, "destroy the group (mhd_group_destroy) first");
+  // peer memory: the neighbours' stores of their last operation into this workspace have landed
+  // before the caller may release it (the caller also barriers across ranks: mesh.py)
+  settle_remote(m);
   cudaStreamSynchronize(m->stream);
   if (m->comm) ncclCommDestroy(m->comm);
   for (void* b : m->ipc_bases) cudaIpcCloseMemHandle(b);
   if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
   if (m->ev_ready) cudaEventDestroy(m->ev_ready);
   if (m->ev_halo) cudaEventDestroy(m->ev_halo);
+  for (int i = 0; i < kRing; ++i) {
+    if (m->ev_arrive[i]) cudaEventDestroy(m->ev_arrive[i]);
+    if (m->ev_done[i]) cudaEventDestroy(m->ev_done[i]);
+  }
   if (m->h_red) cudaFreeHost(m->h_red);
   for (auto& a : m->aio) {
     if (a.st) {
@@ -1120,7 +1317,6 @@ mhd_status mhd_mesh_destroy(mhd_mesh* m) {
   delete m;
   return MHD_OK;
 }
-
 
 mhd_status mhd_load(mhd_mesh* m, int32_t field, const void* src, int32_t src_dtype, int32_t on_device) {
   if (!m || !src || field < 0 || field >= NF) return fail(MHD_EINVAL, "bad load argument");
@@ -1214,41 +1410,29 @@ mhd_status mhd_store_grid(mhd_mesh* m, int32_t field, void* dst, int32_t on_devi
   const char* first = base + (size_t)(m->L.xo - rad) * es;  // (x, y, z) = (-r, -r, -r)
   const size_t mx = (size_t)m->g.nx + 2 * rad, my = (size_t)m->g.ny + 2 * rad;
   const size_t mz = (size_t)m->g.nz + 2 * rad;
+  settle_remote(m);  // the neighbours' stores into this halo have landed (peer-memory exchange)
   CU(cudaMemcpy2DAsync(dst, mx * es, first, (size_t)m->g.sy * es, mx * es, my * mz,
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, m->stream));
-  if (!on_device) CU(cudaStreamSynchronize(m->stream));
+  if (!on_device) {
+    CU(cudaStreamSynchronize(m->stream));
+    return check_spin(m);
+  }
   return MHD_OK;
 }
 
 mhd_status mhd_halo_exchange(mhd_mesh* m) {
   if (!m) return fail(MHD_EINVAL, "null mesh");
-  if (m->exchange == 1) {
-    if (m->info.dtype == MHD_F64) {
-      ensure_self<double>(m);
-      p2p_halo_copy<double>(m);
-    } else {
-      ensure_self<float>(m);
-      p2p_halo_copy<float>(m);
-    }
-    launch_p2p_wait(m->stream, m->my_done, m->seq);  // the neighbours' copies into this halo have landed
-    m->launches += 1;
-    CU(cudaGetLastError());
-    return MHD_OK;
-  }
-  mhd_status st = m->info.dtype == MHD_F64 ? halo_begin<double>(m) : halo_begin<float>(m);
-  if (st != MHD_OK) return st;
-  st = m->info.dtype == MHD_F64 ? halo_end<double>(m) : halo_end<float>(m);
-  if (st != MHD_OK) return st;
-  CU(cudaGetLastError());
-  return MHD_OK;
+  if (in_group(m)) return fail(MHD_EINVAL, "mesh belongs to a group: use mhd_group_halo_exchange");
+  return m->info.dtype == MHD_F64 ? halo_exchange_all<double>(&m, 1) : halo_exchange_all<float>(&m, 1);
 }
 
 mhd_status mhd_integrate_substep(mhd_mesh* m, int32_t k, double dt) {
   if (!m) return fail(MHD_EINVAL, "null mesh");
+  if (in_group(m)) return fail(MHD_EINVAL, "mesh belongs to a group: use mhd_group_integrate_substep");
   if (k < 0 || k > 2) return fail(MHD_EINVAL, "k must be 0, 1 or 2");
   if (k != m->next_k) return fail(MHD_ESTATE, "substeps must run in the order 0, 1, 2");
-  mhd_status st = m->info.dtype == MHD_F64 ? substep_impl<double>(m, k, dt, nullptr)
-                                           : substep_impl<float>(m, k, dt, nullptr);
+  mhd_status st = m->info.dtype == MHD_F64 ? substep_all<double>(&m, 1, k, dt, nullptr)
+                                           : substep_all<float>(&m, 1, k, dt, nullptr);
   if (st != MHD_OK) return st;
   m->cur = 1 - m->cur;
   m->next_k = (k + 1) % 3;
@@ -1265,18 +1449,21 @@ mhd_status mhd_integrate_step(mhd_mesh* m, double dt) {
 
 mhd_status mhd_debug_rhs(mhd_mesh* m, void* dev_dst) {
   if (!m || !dev_dst) return fail(MHD_EINVAL, "null argument");
-  return m->info.dtype == MHD_F64 ? substep_impl<double>(m, 0, 0.0, static_cast<double*>(dev_dst))
-                                  : substep_impl<float>(m, 0, 0.0, static_cast<float*>(dev_dst));
+  if (in_group(m)) return fail(MHD_EINVAL, "mesh belongs to a group: use mhd_group_debug_rhs");
+  if (m->info.dtype == MHD_F64) {
+    double* d = static_cast<double*>(dev_dst);
+    return substep_all<double>(&m, 1, 0, 0.0, &d);
+  }
+  float* d = static_cast<float*>(dev_dst);
+  return substep_all<float>(&m, 1, 0, 0.0, &d);
 }
 
 mhd_status mhd_reduce(mhd_mesh* m, int32_t field, int32_t op, double* out) {
   if (!m || !out || field < 0 || field >= NF || op < 0 || op > MHD_SUM_EXP) return fail(MHD_EINVAL, "bad reduce argument");
+  if (in_group(m)) return fail(MHD_EINVAL, "mesh belongs to a group: use mhd_group_reduce");
+  mhd_status st = reduce_local(m, field, op, false);
+  if (st != MHD_OK) return st;
   double* sc = m->red_scratch();
-  if (m->info.dtype == MHD_F64)
-    launch_reduce<double>(m->stream, m->fields<double>(m->cur).f[field], m->g, sc, kReduceBlocks);
-  else
-    launch_reduce<float>(m->stream, m->fields<float>(m->cur).f[field], m->g, sc, kReduceBlocks);
-  m->launches += 2;
   if (m->distributed()) {
     if (!m->comm) return fail(MHD_ENCCL, "mhd_comm_init was not called");
     NC(ncclGroupStart());
@@ -1287,18 +1474,9 @@ mhd_status mhd_reduce(mhd_mesh* m, int32_t field, int32_t op, double* out) {
   }
   CU(cudaMemcpyAsync(m->h_red, sc, kReduceVals * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
-  const double* v = m->h_red;
-  const double ncell = (double)m->info.n[0] * (double)m->info.n[1] * (double)m->info.n[2];
-  switch (op) {
-    case MHD_MIN: *out = v[0]; break;
-    case MHD_MAX: *out = v[1]; break;
-    case MHD_SUM: *out = v[2]; break;
-    case MHD_RMS: *out = std::sqrt(v[3] / ncell); break;
-    case MHD_SUM_EXP: *out = v[4]; break;
-  }
-  if (!std::isfinite(v[2]) || !std::isfinite(v[3]) || !std::isfinite(v[0]) || !std::isfinite(v[1]))
-    return fail(MHD_ENONFINITE, "field holds a NaN or Inf");
-  return MHD_OK;
+  st = check_spin(m);
+  if (st != MHD_OK) return st;
+  return reduce_finish(m->h_red, m->info, op, out);
 }
 
 mhd_status mhd_synchronize(mhd_mesh* m) {
@@ -1308,7 +1486,7 @@ mhd_status mhd_synchronize(mhd_mesh* m) {
   for (auto& a : m->aio)
     if (a.st) CU(cudaStreamSynchronize(a.st));
   CU(cudaGetLastError());
-  return MHD_OK;
+  return check_spin(m);
 }
 
 mhd_status mhd_set_kernel(mhd_mesh* m, int32_t variant) {
@@ -1319,6 +1497,12 @@ mhd_status mhd_set_kernel(mhd_mesh* m, int32_t variant) {
     if (!ok) return fail(MHD_EUNSUPPORTED, "z-marching kernel does not support this geometry");
   }
   m->variant = variant;
+  return MHD_OK;
+}
+
+mhd_status mhd_set_debug(mhd_mesh* m, int32_t flags) {
+  if (!m || (flags & ~MHD_DEBUG_POISON_HALO)) return fail(MHD_EINVAL, "unknown debug flag");
+  m->debug = flags;
   return MHD_OK;
 }
 
@@ -1361,6 +1545,7 @@ mhd_status mhd_p2p_export(mhd_mesh* m, void* out_blob) {
 mhd_status mhd_p2p_open(mhd_mesh* m, const void* blobs) {
   if (!m || !blobs) return fail(MHD_EINVAL, "null argument");
   if (m->info.nranks == 1) return MHD_OK;
+  if (in_group(m)) return fail(MHD_EINVAL, "mesh belongs to a group");
   if (m->peers.size() > (size_t)kMaxPeers) return fail(MHD_EUNSUPPORTED, "more than 7 neighbours");
   CU(cudaStreamSynchronize(m->stream));  // the zeroed flags are in place before anyone signals
   m->peer_ws.assign(m->info.nranks, nullptr);
@@ -1379,52 +1564,175 @@ mhd_status mhd_p2p_open(mhd_mesh* m, const void* blobs) {
     m->ipc_bases.push_back(base);
     m->peer_ws[p.peer] = static_cast<char*>(base) + off;
   }
-  memset(&m->peer_arrive, 0, sizeof(FlagSet));
-  memset(&m->peer_done, 0, sizeof(FlagSet));
-  memset(&m->my_arrive, 0, sizeof(FlagSet));
-  memset(&m->my_done, 0, sizeof(FlagSet));
-  const int nr = m->info.nranks;
-  for (auto& p : m->peers) {
-    unsigned long long* peer_flags = reinterpret_cast<unsigned long long*>(m->peer_ws[p.peer] + m->L.flags_off);
-    unsigned long long* my_flags = reinterpret_cast<unsigned long long*>(m->ws + m->L.flags_off);
-    m->peer_arrive.ptr[m->peer_arrive.n++] = peer_flags + m->info.rank;
-    m->peer_done.ptr[m->peer_done.n++] = peer_flags + nr + m->info.rank;
-    m->my_arrive.ptr[m->my_arrive.n++] = my_flags + p.peer;
-    m->my_done.ptr[m->my_done.n++] = my_flags + nr + p.peer;
-  }
-  // remote segments (buf_off = peer slot) for the halo copy of a freshly loaded state
-  memset(&m->remote_list, 0, sizeof(m->remote_list));
-  int nb = 0;
-  for (auto& si : m->segs) {
-    if (si.self) continue;
-    SegDesc& d = m->remote_list.s[m->remote_list.n++];
-    for (int a = 0; a < 3; ++a) {
-      d.src[a] = si.s.src_first[a];
-      d.dst[a] = si.s.dst_first[a];
-      d.ext[a] = si.s.extent[a];
-    }
-    d.count = (long long)d.ext[0] * d.ext[1] * d.ext[2];
-    for (size_t i = 0; i < m->peers.size(); ++i)
-      if (m->peers[i].peer == si.s.send_peer) d.buf_off = (long long)i;
-    d.block0 = nb;
-    nb += (int)((d.count + 255) / 256);
-  }
-  m->remote_list.nblocks = nb;
+  mhd_status st = open_peers(m);
+  if (st != MHD_OK) return st;
   m->exchange = 1;
+  return MHD_OK;
+}
+
+mhd_status mhd_set_exchange(mhd_mesh* m, int32_t mode) {
+  if (!m || mode < 0 || mode > 1) return fail(MHD_EINVAL, "mode must be 0 (packed / NCCL) or 1 (peer memory)");
+  if (in_group(m)) return fail(MHD_EINVAL, "mesh belongs to a group: the group fixes the exchange");
+  if (mode == 1 && m->info.nranks > 1 && m->peer_ws.empty()) return fail(MHD_EINVAL, "mhd_p2p_open first");
+  if (mode == 0 && m->info.nranks > 1 && !m->comm) return fail(MHD_ENCCL, "mhd_comm_init first");
+  settle_remote(m);
+  m->exchange = m->info.nranks > 1 ? mode : 0;
   m->halo_valid = false;
   m->self_valid = false;
   m->x_valid = false;
   return MHD_OK;
 }
 
-mhd_status mhd_set_exchange(mhd_mesh* m, int32_t mode) {
-  if (!m || mode < 0 || mode > 1) return fail(MHD_EINVAL, "mode must be 0 (NCCL) or 1 (peer memory)");
-  if (mode == 1 && m->info.nranks > 1 && m->peer_ws.empty()) return fail(MHD_EINVAL, "mhd_p2p_open first");
-  if (mode == 0 && m->info.nranks > 1 && !m->comm) return fail(MHD_ENCCL, "mhd_comm_init first");
-  m->exchange = m->info.nranks > 1 ? mode : 0;
-  m->halo_valid = false;
-  m->self_valid = false;
-  m->x_valid = false;
+// ---- several ranks in one process ------------------------------------------------------------------
+
+mhd_status mhd_group_create(mhd_mesh* const* meshes, int32_t n, int32_t exchange, mhd_group** out) {
+  if (!meshes || !out || n < 1 || exchange < 0 || exchange > 1) return fail(MHD_EINVAL, "bad group argument");
+  for (int i = 0; i < n; ++i) {
+    const mhd_mesh* m = meshes[i];
+    if (!m) return fail(MHD_EINVAL, "null mesh");
+    if (m->info.nranks != n || m->info.rank != i) return fail(MHD_EINVAL, "meshes must be ranks 0..n-1 of an n-rank mesh, in order");
+    if (m->group || m->comm || !m->peer_ws.empty()) return fail(MHD_EINVAL, "mesh already has a communicator or group");
+    for (int a = 0; a < 3; ++a)
+      if (m->info.n[a] != meshes[0]->info.n[a]) return fail(MHD_EINVAL, "meshes of different grids");
+    if (m->info.dtype != meshes[0]->info.dtype || m->info.radius != meshes[0]->info.radius ||
+        m->info.exchange_corners != meshes[0]->info.exchange_corners)
+      return fail(MHD_EINVAL, "meshes of different dtype, radius or corner setting");
+    if (exchange == 1 && m->peers.size() > (size_t)kMaxPeers) return fail(MHD_EUNSUPPORTED, "more than 7 neighbours");
+  }
+  int dev0 = 0;
+  CU(cudaGetDevice(&dev0));
+  // peer access between the devices of neighbouring ranks (ranks on one device need none)
+  for (int i = 0; i < n; ++i)
+    for (auto& p : meshes[i]->peers) {
+      const int a = meshes[i]->device, b = meshes[p.peer]->device;
+      if (a == b) continue;
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) return fail(MHD_EUNSUPPORTED, "group: devices without peer access");
+      CU(cudaSetDevice(a));
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return fail(MHD_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+    }
+  mhd_group* g = new mhd_group();
+  g->exchange = exchange;
+  for (int i = 0; i < n; ++i) {
+    mhd_mesh* m = meshes[i];
+    CU(cudaSetDevice(m->device));
+    CU(cudaStreamSynchronize(m->stream));
+    for (int j = 0; j < kRing; ++j) {
+      if (!m->ev_arrive[j]) CU(cudaEventCreateWithFlags(&m->ev_arrive[j], cudaEventDisableTiming));
+      if (!m->ev_done[j]) CU(cudaEventCreateWithFlags(&m->ev_done[j], cudaEventDisableTiming));
+    }
+    m->peer_ws.assign(n, nullptr);
+    for (auto& p : m->peers) m->peer_ws[p.peer] = meshes[p.peer]->ws;
+    g->m.push_back(m);
+  }
+  for (auto* m : g->m) {
+    mhd_status st = open_peers(m);
+    if (st != MHD_OK) {
+      delete g;
+      return st;
+    }
+    m->group = g;
+    m->exchange = exchange;
+    m->seq = 0;
+  }
+  CU(cudaSetDevice(dev0));
+  *out = g;
+  return MHD_OK;
+}
+
+mhd_status mhd_group_destroy(mhd_group* g) {
+  if (!g) return MHD_OK;
+  for (auto* m : g->m) {
+    cudaSetDevice(m->device);
+    cudaStreamSynchronize(m->stream);
+    if (m->comm_stream) cudaStreamSynchronize(m->comm_stream);
+  }
+  for (auto* m : g->m) {
+    m->group = nullptr;
+    m->peer_ws.clear();
+    m->exchange = 0;
+  }
+  delete g;
+  return MHD_OK;
+}
+
+mhd_status mhd_group_halo_exchange(mhd_group* g) {
+  if (!g) return fail(MHD_EINVAL, "null group");
+  mhd_mesh* const* ms = g->m.data();
+  const int n = (int)g->m.size();
+  return ms[0]->info.dtype == MHD_F64 ? halo_exchange_all<double>(ms, n) : halo_exchange_all<float>(ms, n);
+}
+
+mhd_status mhd_group_integrate_substep(mhd_group* g, int32_t k, double dt) {
+  if (!g) return fail(MHD_EINVAL, "null group");
+  if (k < 0 || k > 2) return fail(MHD_EINVAL, "k must be 0, 1 or 2");
+  for (auto* m : g->m)
+    if (k != m->next_k) return fail(MHD_ESTATE, "substeps must run in the order 0, 1, 2 on every rank");
+  mhd_mesh* const* ms = g->m.data();
+  const int n = (int)g->m.size();
+  mhd_status st = ms[0]->info.dtype == MHD_F64 ? substep_all<double>(ms, n, k, dt, nullptr)
+                                               : substep_all<float>(ms, n, k, dt, nullptr);
+  if (st != MHD_OK) return st;
+  for (auto* m : g->m) {
+    m->cur = 1 - m->cur;
+    m->next_k = (k + 1) % 3;
+  }
+  return MHD_OK;
+}
+
+mhd_status mhd_group_integrate_step(mhd_group* g, double dt) {
+  for (int k = 0; k < 3; ++k) {
+    mhd_status st = mhd_group_integrate_substep(g, k, dt);
+    if (st != MHD_OK) return st;
+  }
+  return MHD_OK;
+}
+
+mhd_status mhd_group_debug_rhs(mhd_group* g, void* const* dev_dst) {
+  if (!g || !dev_dst) return fail(MHD_EINVAL, "null argument");
+  mhd_mesh* const* ms = g->m.data();
+  const int n = (int)g->m.size();
+  if (ms[0]->info.dtype == MHD_F64)
+    return substep_all<double>(ms, n, 0, 0.0, reinterpret_cast<double* const*>(dev_dst));
+  return substep_all<float>(ms, n, 0, 0.0, reinterpret_cast<float* const*>(dev_dst));
+}
+
+mhd_status mhd_group_reduce(mhd_group* g, int32_t field, int32_t op, double* out) {
+  if (!g || !out || field < 0 || field >= NF || op < 0 || op > MHD_SUM_EXP) return fail(MHD_EINVAL, "bad reduce argument");
+  int dev0 = 0;
+  CU(cudaGetDevice(&dev0));
+  for (auto* m : g->m) {
+    CU(cudaSetDevice(m->device));
+    mhd_status st = reduce_local(m, field, op, true);
+    if (st != MHD_OK) return st;
+  }
+  double v[kReduceVals] = {INFINITY, -INFINITY, 0.0, 0.0, 0.0};
+  for (auto* m : g->m) {  // combined in rank order on the host
+    CU(cudaSetDevice(m->device));
+    CU(cudaStreamSynchronize(m->stream));
+    const double* h = m->h_red;
+    v[0] = std::fmin(v[0], h[0]);
+    v[1] = std::fmax(v[1], h[1]);
+    for (int j = 2; j < kReduceVals; ++j) v[j] += h[j];
+    if (std::isnan(h[0]) || std::isnan(h[1])) v[2] = NAN;
+  }
+  CU(cudaSetDevice(dev0));
+  return reduce_finish(v, g->m[0]->info, op, out);
+}
+
+mhd_status mhd_group_synchronize(mhd_group* g) {
+  if (!g) return fail(MHD_EINVAL, "null group");
+  int dev0 = 0;
+  CU(cudaGetDevice(&dev0));
+  for (auto* m : g->m) {
+    CU(cudaSetDevice(m->device));
+    mhd_status st = mhd_synchronize(m);
+    if (st != MHD_OK) return st;
+  }
+  CU(cudaSetDevice(dev0));
   return MHD_OK;
 }
 

@@ -62,28 +62,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 // refills the ring.  Measured (256^3, one B200): +15 % for the FP64 order-8 kernel (32x4 tile,
 // 4 warps per SM); slower with 8 warps per SM (-12 % FP64 / -17 % FP32 at order 6, -15 % FP32 at
 // order 8), so only the 4-row tiles use it.
-#ifndef B2_ZM_TQ
-#define B2_ZM_TQ 0
-#endif
-// tensor-memory z queue helpers (ZCfg::TQ)
-__device__ __forceinline__ void tq_ld4(unsigned addr, double (&v)[4]) {
-  unsigned r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(addr));
-  // the wait is tied to the loaded registers (not a memory clobber), so that the compiler may
-  // still move shared-memory loads across it
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
-#pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
-}
-__device__ __forceinline__ void tq_st1(unsigned addr, double v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(addr),
-               "r"((unsigned)__double2loint(v)), "r"((unsigned)__double2hiint(v)));
-}
-__device__ __forceinline__ void tq_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-
 __device__ __forceinline__ void bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
@@ -111,10 +89,6 @@ struct ZCfg {
   static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128 + 16;
   static constexpr bool FITS = SMEM <= 227 * 1024;
   static constexpr bool SKEW = TY < 8;  // the 4-row tiles (FP64, r = 4)
-  // z queue in tensor memory (B2_ZM_TQ): the centres of planes o..o+2 of every field are kept per
-  // thread in TMEM (tcgen05.st / tcgen05.ld, 32x32b shape) instead of being re-read from the ring
-  // as the z taps of three successive outputs (FP64, r = 3)
-  static constexpr bool TQ = B2_ZM_TQ && sizeof(T) == 8 && RAD == 3 && !SKEW;
 };
 
 // Register state carried along z by one thread.
@@ -124,7 +98,7 @@ struct March {
   T acc[2][RAD][3];  // [u|A][logical output o .. o+r-1 -> physical (j + PH) % r][z-part of x_0, x_1, x_2]
 };
 
-template <typename T, int RAD, int MODE, bool REMOTE>
+template <typename T, int RAD, int MODE>
 struct ZStep {
   using Z = ZCfg<T, RAD>;
   const T* ring;
@@ -133,54 +107,7 @@ struct ZStep {
   int cell;   // offset of this thread's cell inside a field of a slot
   int pcell;  // offset inside a field of the f_{k-1} tile
   int slot0;  // plane zb - r (first staged plane) has slot 0
-  const RemoteMap<T>& rm;
   bool lead;  // leading warp group (ZCfg::SKEW): signals "past the loads of plane o" mid-iteration
-  unsigned tq;  // ZCfg::TQ: tensor-memory address of this thread's z queue (lane, column group)
-
-  // queue slot of plane o + i at phase PH is (i + PH) % 3; field q owns columns 8q .. 8q + 5
-  template <int PH>
-  __device__ __forceinline__ void zq_get(int q, T (&z)[3]) const {
-    double v[4];
-    tq_ld4(tq + 8u * (unsigned)q, v);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) z[i] = v[(i + PH) % 3];
-  }
-  template <int PH>
-  __device__ __forceinline__ void zq_put(int q, T val) const {
-    tq_st1(tq + 8u * (unsigned)q + 2u * (unsigned)(PH % 3), val);
-  }
-  // z derivatives of field q at output o from the queue (o, o+1, o+2), the ring (o+3) and the
-  // register history (o-3 .. o-1); the same arithmetic as axis_z
-  template <int PH>
-  __device__ __forceinline__ void axis_zq(const March<T, RAD>& st, int q, T f0, const T (&zp)[RAD], T& d1,
-                                          T& d2) const {
-    T dl[RAD], sg[RAD];
-#pragma unroll
-    for (int i = 1; i <= RAD; ++i) {
-      const T p = zp[i - 1], m = st.hist[q][(RAD - i + PH) % RAD];
-      dl[i - 1] = p - m;
-      sg[i - 1] = p + m;
-    }
-    d1 = d1_of<T, RAD>(dl, C.c1[2]);
-    d2 = d2_of<T, RAD>(f0, sg, C.d2[2], C.d0[2]);
-  }
-  // centre of field q at output plane o, with its z derivatives; pushes plane o+3 into the queue
-  template <int PH>
-  __device__ __forceinline__ T centre_z(const March<T, RAD>& st, int q, const T* const (&sk)[RAD + 1], T& d1,
-                                        T& d2) const {
-    if constexpr (Z::TQ) {
-      T z[3];
-      zq_get<PH>(q, z);
-      const T zp[RAD] = {z[1], z[2], at(sk[RAD], q, 0, 0)};
-      zq_put<PH>(q, zp[RAD - 1]);
-      axis_zq<PH>(st, q, z[0], zp, d1, d2);
-      return z[0];
-    } else {
-      const T f0 = at(sk[0], q, 0, 0);
-      axis_z<PH>(st, q, f0, sk, d1, d2);
-      return f0;
-    }
-  }
 
   __device__ __forceinline__ void signal_half(int o) const {
     if (Z::SKEW && lead) bar_arrive(1 + (o & 1), Z::NT);
@@ -276,11 +203,6 @@ struct ZStep {
     }
 #pragma unroll
     for (int q = 0; q < NF; ++q) st.hist[q][(0 + PH) % RAD] = at(s0, q, 0, 0);
-    if constexpr (Z::TQ) {
-      const T* s3 = slot_of(p + RAD);
-#pragma unroll
-      for (int q = 0; q < NF; ++q) zq_put<PH>(q, at(s3, q, 0, 0));
-    }
     signal_half(p);
   }
 
@@ -296,14 +218,9 @@ struct ZStep {
     for (int c = 0; c < 3; ++c) {
       const int q = qx + c;
       T d1a[2], d2a[2];
-      if constexpr (Z::TQ) {
-        f[c] = centre_z<PH>(st, q, sk, g[c][2], d2[c][2]);
-        axis_xy(s0, q, f[c], d1a, d2a, dlx[c], dly[c]);
-      } else {
-        f[c] = at(s0, q, 0, 0);
-        axis_xy(s0, q, f[c], d1a, d2a, dlx[c], dly[c]);
-        axis_z<PH>(st, q, f[c], sk, g[c][2], d2[c][2]);
-      }
+      f[c] = at(s0, q, 0, 0);
+      axis_xy(s0, q, f[c], d1a, d2a, dlx[c], dly[c]);
+      axis_z<PH>(st, q, f[c], sk, g[c][2], d2[c][2]);
       g[c][0] = d1a[0];
       g[c][1] = d1a[1];
       d2[c][0] = d2a[0];
@@ -349,14 +266,9 @@ struct ZStep {
     for (int h = 0; h < 2; ++h) {
       const int q = h == 0 ? LNRHO : SS;
       T d1a[2], d2a[2], dlx[RAD], dly[RAD], d2z;
-      if constexpr (Z::TQ) {
-        sc[h] = centre_z<PH>(st, q, sk, gsc[h][2], d2z);
-        axis_xy(sk[0], q, sc[h], d1a, d2a, dlx, dly);
-      } else {
-        sc[h] = at(sk[0], q, 0, 0);
-        axis_xy(sk[0], q, sc[h], d1a, d2a, dlx, dly);
-        axis_z<PH>(st, q, sc[h], sk, gsc[h][2], d2z);
-      }
+      sc[h] = at(sk[0], q, 0, 0);
+      axis_xy(sk[0], q, sc[h], d1a, d2a, dlx, dly);
+      axis_z<PH>(st, q, sc[h], sk, gsc[h][2], d2z);
       gsc[h][0] = d1a[0];
       gsc[h][1] = d1a[1];
       lap[h] = (d2a[0] + d2a[1]) + d2z;
@@ -374,8 +286,7 @@ struct ZStep {
           fn[q] = rk_update<T>(k, fk[q], k > 0 ? pv[q * Z::PSZ] : (T)0, rhs[q], C);
           out.f[q][gidx] = fn[q];
         }
-        if (REMOTE) remote_store<T, RAD>(rm, g.nx, g.ny, g.nz, g.sy, g.sz, x, y, o, fn);
-        if (!REMOTE && g.xwrap) {
+        if (g.xwrap) {
           // periodic x faces of this rank's own halo (x unsplit) written here: the cells in
           // the first / last 32-byte sector of a row also go to the row padding on the other side
           // (whole sectors: the extra cell lands in unused padding).  (Adding the y faces here
@@ -407,10 +318,10 @@ __device__ __forceinline__ void unroll_phases(F&& f, int p, int ze) {
   }
 }
 
-template <typename T, int RAD, int MODE, bool REMOTE>
+template <typename T, int RAD, int MODE>
 __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C,
-                  int k, T* __restrict__ rhs_out, int nzc, int xo, const __grid_constant__ RemoteMap<T> rm, int persist) {
+                  int k, T* __restrict__ rhs_out, int nzc, int xo, int persist) {
   using Z = ZCfg<T, RAD>;
   constexpr int TX = Z::TX, TY = Z::TY;
   // Dynamic shared memory starts at the (1024-B aligned) base of the CTA window (no static
@@ -430,20 +341,6 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     if (smem_u32(smem_raw) & 127) __trap();  // TMA destinations need 128-B alignment
     for (int s = 0; s < Z::NSLOT; ++s) mbar_init(&mbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  unsigned tq = 0;
-  if constexpr (Z::TQ) {
-    // 128 TMEM columns: 2 column groups (warps w and w + 4 share a lane quadrant) x 8 fields x 8
-    uint32_t* const tbase = reinterpret_cast<uint32_t*>(mbar + Z::NSLOT);
-    if (tid < 32) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_u32(tbase)));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const int warp = tid / 32;
-    tq = *tbase + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)((warp >> 2) * 64);
   }
   __syncthreads();
 
@@ -479,8 +376,8 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
       mbar_wait(&mbar[rel % Z::NSLOT], (rel / Z::NSLOT) & 1u);
     };
 
-    const ZStep<T, RAD, MODE, REMOTE> S{ring, prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
-                                        first - (int)(base % Z::NSLOT), rm, lead, tq};
+    const ZStep<T, RAD, MODE> S{ring, prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
+                                        first - (int)(base % Z::NSLOT), lead};
     March<T, RAD> st;
 #pragma unroll
     for (int v = 0; v < 2; ++v)
@@ -508,7 +405,6 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
         issue(p + RAD + 1);
       }
       wait_plane(p + RAD);  // plane p+r and f_{k-1}(p) have landed
-      if constexpr (Z::TQ) tq_wait_st();  // last iteration's queue store is visible to its loads
       if (p < zb)
         S.template push_only<PH>(st, p);
       else
@@ -543,33 +439,26 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
     u += zlen;
     if (u < u1) __syncthreads();  // every thread is done with the ring before the next prologue
   }
-  if constexpr (Z::TQ) {
-    tq_wait_st();
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    if (tid < 32) {
-      uint32_t* const tbase = reinterpret_cast<uint32_t*>(mbar + Z::NSLOT);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(*tbase));
-    }
-  }
-  if (REMOTE && rm.sys) __threadfence_system();  // peer halo stores visible before the completion signal
 }
 
 constexpr int kNZC = 64;
 
-template <typename T, int RAD, int MODE, bool REMOTE>
+template <typename T, int RAD, int MODE>
 void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>& rm, bool persist, int zchunk) {
+                const Coef<T>& C, int k, T* rhs_out, int xo, bool persist, int zchunk) {
   using Z = ZCfg<T, RAD>;
-  static int resident = 0;  // CTAs of this instantiation that fit on the GPU at once
+  // CTAs of this instantiation that fit on the GPU at once, per device (one process may drive several
+  // devices: mhd_group_*); the >48 KB dynamic shared memory attribute is set on each device's first use
+  static int resident_of[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& resident = resident_of[dev & 63];
   if (!resident) {
-    cudaFuncSetAttribute(zmarch_kernel<T, RAD, MODE, REMOTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(zmarch_kernel<T, RAD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Z::SMEM);
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, zmarch_kernel<T, RAD, MODE, REMOTE>, Z::NT, Z::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, zmarch_kernel<T, RAD, MODE>, Z::NT, Z::SMEM);
     resident = std::max(1, sms * std::max(1, per));
   }
   const int cz = zchunk > 0 ? zchunk : kNZC;
@@ -579,7 +468,7 @@ void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const 
   // skew, whose barrier ids follow the plane parity, is off)
   const bool pers = persist && !Z::SKEW && (long long)grd.x * grd.y * grd.z > resident;
   if (pers) grd = dim3(resident, 1, 1);
-  zmarch_kernel<T, RAD, MODE, REMOTE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, rm, pers ? 1 : 0);
+  zmarch_kernel<T, RAD, MODE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, pers ? 1 : 0);
 }
 
 }  // namespace zm
@@ -592,22 +481,18 @@ bool zmarch_supported(const Geom& g, const Region& r) {
 
 template <typename T, int RAD>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
-                   const Coef<T>& C, int k, T* rhs_out, int xo, const RemoteMap<T>* rm, bool persist,
-                   int zchunk) {
+                   const Coef<T>& C, int k, T* rhs_out, int xo, bool persist, int zchunk) {
   if constexpr (zm::ZCfg<T, RAD>::FITS) {
-    RemoteMap<T> none;
     if (rhs_out)
-      zm::launch_cfg<T, RAD, 1, false>(st, tm, out, g, r, C, k, rhs_out, xo, none, persist, zchunk);
-    else if (rm)
-      zm::launch_cfg<T, RAD, 0, true>(st, tm, out, g, r, C, k, nullptr, xo, *rm, persist, zchunk);
+      zm::launch_cfg<T, RAD, 1>(st, tm, out, g, r, C, k, rhs_out, xo, persist, zchunk);
     else
-      zm::launch_cfg<T, RAD, 0, false>(st, tm, out, g, r, C, k, nullptr, xo, none, persist, zchunk);
+      zm::launch_cfg<T, RAD, 0>(st, tm, out, g, r, C, k, nullptr, xo, persist, zchunk);
   }
 }
 
 #define B2_ZMARCH_INSTANTIATE(T, RAD)                                                                      \
   template bool zmarch_supported<T, RAD>(const Geom&, const Region&);                                       \
   template void launch_zmarch<T, RAD>(cudaStream_t, const TmapSet&, const Fields<T>&, const Geom&, const Region&, \
-                                      const Coef<T>&, int, T*, int, const RemoteMap<T>*, bool, int);
+                                      const Coef<T>&, int, T*, int, bool, int);
 
 }  // namespace b2

@@ -95,37 +95,53 @@ def test_halo_exchange_sentinel_bitwise(corners, n):
     m.close()
 
 
-@pytest.mark.parametrize("corners", [False, True])
-@pytest.mark.parametrize("n,r", [((40, 24, 19), 3), ((37, 23, 16), 1), ((36, 20, 18), 4)])
-def test_wrap_store_halo_bitwise(corners, n, r, monkeypatch):
-    """After substeps (no explicit exchange) the halo of the new state, written by the update
-    kernel's epilogue (wrap stores), is the periodic wrap of its interior, bitwise.  (One
-    rank uses the self-copy by default; B2MHD_WRAP=1 forces the wrap stores.)"""
-    monkeypatch.setenv("B2MHD_WRAP", "1")
-    m, _ = _mesh(n, exchange_corners=corners, radius=r)
-    st = synth.pcg64_state((n[2], n[1], n[0]))
+@pytest.mark.parametrize("dtype", [8, 4])
+@pytest.mark.parametrize("n,r", [((40, 24, 19), 3), ((37, 23, 16), 1), ((36, 20, 18), 4), ((64, 48, 40), 3),
+                                 ((12, 20, 16), 3)])
+def test_poison_halo_steps_bit_identical(dtype, n, r):
+    """NaN-poison mode (MHD_DEBUG_POISON_HALO): before every update each halo cell of the state it
+    writes is NaN, and each loaded field's halo too.  One rank keeps its halo by three mechanisms
+    (x faces from the update epilogue, y rows copied, z planes fetched through the TMA coordinate
+    wrap and never stored) and never exchanges corners: if any stencil read a cell
+    none of them refreshed, NaN would spread.  The state after 2 RK3 steps is bit-identical to the
+    run without poison (nx = 12: the direct kernel)."""
+    import paper_2103_01597_b200 as b2
+    st = synth.pcg64_state((n[2], n[1], n[0]), dtype=np.float64 if dtype == 8 else np.float32)
+    outs = []
+    for debug in (0, b2.MHD_DEBUG_POISON_HALO):
+        m, _ = _mesh(n, radius=r, dtype=dtype)
+        m.set_debug(debug)
+        m.load(st)
+        for _ in range(2):
+            m.step(1e-4)
+        outs.append(m.store().cpu().numpy())
+        if debug:  # the poison is really there: the corners of the current state are NaN
+            grid = m.store_grid().numpy()
+            assert np.all(np.isnan(grid[:, :r, :r, :r]))
+        m.close()
+    assert np.all(np.isfinite(outs[1]))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_poison_halo_exchange_bitwise():
+    """With the poison on, an explicit exchange refills every non-corner halo cell bitwise."""
+    import paper_2103_01597_b200 as b2
+    n = (37, 23, 19)
+    m, _ = _mesh(n)
+    m.set_debug(b2.MHD_DEBUG_POISON_HALO)
+    nz, ny, nx = n[2], n[1], n[0]
+    st = (np.arange(8)[:, None, None, None] * 1e6 + np.arange(nz * ny * nx).reshape(nz, ny, nx)).astype(np.float64)
     m.load(st)
-    for k in range(3):
-        m.substep(k, 1e-3)
-        grid = m.store_grid().numpy()
-        expect = np.stack([oracle.periodic_fill(oracle.with_halo(grid[q][r:-r, r:-r, r:-r], r), r=r)
-                           for q in range(8)])
-        mask = np.ones(grid.shape[1:], bool)
-        if not corners:
-            for zs in (slice(0, r), slice(-r, None)):
-                for ys in (slice(0, r), slice(-r, None)):
-                    for xs in (slice(0, r), slice(-r, None)):
-                        mask[zs, ys, xs] = False
-        assert np.array_equal(grid[:, mask], expect[:, mask]), k
-    wrapped = m.store().cpu().numpy()
-    m.close()
-    # the same substeps with the self-copy instead: bit-identical state
-    monkeypatch.setenv("B2MHD_WRAP", "0")
-    m, _ = _mesh(n, exchange_corners=corners, radius=r)
-    m.load(st)
-    for k in range(3):
-        m.substep(k, 1e-3)
-    assert np.array_equal(m.store().cpu().numpy(), wrapped)
+    m.halo_exchange()
+    grid = m.store_grid().numpy()
+    expect = np.stack([oracle.periodic_fill(oracle.with_halo(st[q])) for q in range(8)])
+    mask = np.ones(grid.shape[1:], bool)
+    for zs in (slice(0, 3), slice(-3, None)):
+        for ys in (slice(0, 3), slice(-3, None)):
+            for xs in (slice(0, 3), slice(-3, None)):
+                mask[zs, ys, xs] = False
+    assert np.array_equal(grid[:, mask], expect[:, mask])
+    assert np.all(np.isnan(grid[:, ~mask]))
     m.close()
 
 
