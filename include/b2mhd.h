@@ -239,7 +239,9 @@ mhd_status mhd_synchronize(mhd_mesh* mesh);
 /* ---- configuration and introspection --------------------------------------- */
 
 /* Update kernel: 0 = auto (fastest), 1 = direct (one thread per cell, loads via
- * the read-only path), 2 = z-marching shared-memory kernel. */
+ * the read-only path), 2 = z-marching shared-memory kernel, 3 = warp-specialised z-marching
+ * kernel (two threads per cell: magnetic and flow warp groups; FP64, radius 3 only, else
+ * MHD_EUNSUPPORTED).  Every variant gives bit-identical results. */
 mhd_status mhd_set_kernel(mhd_mesh* mesh, int32_t variant);
 
 /* Local geometry of the mesh: P, coord, local n', and the substep counter. */

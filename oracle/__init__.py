@@ -59,6 +59,7 @@ def _lib(kind: str = "d"):
         lib.oracle_real_bytes.restype = ctypes.c_int
         lib.oracle_grid_cells.restype = ctypes.c_size_t
         lib.oracle_integrate.restype = ctypes.c_int
+        lib.oracle_integrate_w2.restype = ctypes.c_int
         lib.oracle_rhs_of_state.restype = ctypes.c_int
         _libs[kind] = lib
     return _libs[kind]
@@ -143,16 +144,19 @@ def rhs(state: np.ndarray, ds, params, kind: str = "d", r: int = R) -> np.ndarra
 
 
 def integrate(state: np.ndarray, ds, params, dt: float, nsteps: int, substeps: int | None = None,
-              kind: str = "d", return_rhs: bool = False, r: int = R):
+              kind: str = "d", return_rhs: bool = False, r: int = R, form: str = "w"):
     """Run nsteps RK3 steps (or exactly `substeps` substeps) from an interior state (8, nz, ny, nx).
 
+    form "w": the explicit 2N register (the definition, R#3); "w2": the algebraically
+    identical two-state form of reading R#4 (only to attribute rounding differences).
     Returns the new state (and the RHS of the last substep if return_rhs).
     """
     st = [np.array(state[q], dtype=_dtype(kind), order="C", copy=True) for q in range(NF)]
     nz, ny, nx = st[0].shape
     rh = [np.empty((nz, ny, nx), dtype=_dtype(kind)) for _ in range(NF)]
     p = _params(params)
-    rc = _lib(kind).oracle_integrate(_ptrs(st), nx, ny, nz, r, _ds(ds), ctypes.byref(p), ctypes.c_double(dt),
+    fn = _lib(kind).oracle_integrate if form == "w" else _lib(kind).oracle_integrate_w2
+    rc = fn(_ptrs(st), nx, ny, nz, r, _ds(ds), ctypes.byref(p), ctypes.c_double(dt),
                                      int(nsteps), -1 if substeps is None else int(substeps), _ptrs(rh))
     if rc != 0:
         raise MemoryError("oracle_integrate")

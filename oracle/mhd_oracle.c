@@ -307,14 +307,36 @@ void oracle_rk3_linear(real* y, size_t n, double lambda, double dt, int nsteps) 
   free(w); free(rhs);
 }
 
+/* The same 2N scheme in the two-state form of reading R#4 (the form the GPU path stores): with
+ * w_k = (f_{k+1} - f_k) / beta_k eliminated,
+ *   f_{k+1} = f_k + (beta_k alpha_k / beta_{k-1}) (f_k - f_{k-1}) + beta_k dt RHS(f_k),
+ * evaluated as t = fma(beta_k dt, RHS, f_k); f_{k+1} = fma(beta_k alpha_k / beta_{k-1}, f_k - f_{k-1}, t).
+ * Algebraically identical to oracle_rk3_update (R(z) pinned in tests); it differs only in rounding,
+ * and exists to attribute the last ulps of the GPU/oracle difference to the form. */
+#ifdef ORACLE_LONG_DOUBLE
+#define FMA fmal
+#else
+#define FMA fma
+#endif
+void oracle_rk3_update_w2(real* f, real* fprev, const real* rhs, size_t n, int k, double dt) {
+  const real b = (real)((double)RK_BETA[k] * dt);
+  const real a = k == 0 ? 0 : (real)((double)RK_BETA[k] * (double)RK_ALPHA[k] / (double)RK_BETA[k - 1]);
+  for (size_t i = 0; i < n; ++i) {
+    const real t = FMA(b, rhs[i], f[i]);
+    const real fn = k == 0 ? t : FMA(a, f[i] - fprev[i], t);
+    fprev[i] = f[i];
+    f[i] = fn;
+  }
+}
+
 /* ---- one full integration: nsteps RK3 steps of the MHD system --------------
  * state: 8 interior arrays (nz*ny*nx, x fastest), updated in place.
  * stop_substep: if >= 0, stop after that many substeps in total (for substep-level
  * parity), else run 3*nsteps substeps.
  * rhs_out: optional 8 interior arrays receiving the RHS of the last substep run. */
-int oracle_integrate(real* const state[NF], int nx, int ny, int nz, int r, const double ds[3],
-                     const oracle_params* p, double dt, int nsteps, int stop_substep,
-                     real* const rhs_out[NF]) {
+static int integrate_form(real* const state[NF], int nx, int ny, int nz, int r, const double ds[3],
+                          const oracle_params* p, double dt, int nsteps, int stop_substep,
+                          real* const rhs_out[NF], int form) {
   size_t ncell = (size_t)nx * ny * nz, ngrid = oracle_grid_cells(nx, ny, nz, r);
   dims3 d = {nx, ny, nz, r};
   const int R = r;
@@ -335,12 +357,29 @@ int oracle_integrate(real* const state[NF], int nx, int ny, int nz, int r, const
       oracle_periodic_fill(f[q], nx, ny, nz, r);     /* halo exchange */
     }
     oracle_rhs(f, nx, ny, nz, r, ds, p, rhs);          /* all cells before any update */
-    for (int q = 0; q < NF; ++q) oracle_rk3_update(state[q], w[q], rhs[q], ncell, k, dt);
+    for (int q = 0; q < NF; ++q) {
+      if (form == 0)
+        oracle_rk3_update(state[q], w[q], rhs[q], ncell, k, dt);
+      else  /* w holds f_{k-1} in the two-state form */
+        oracle_rk3_update_w2(state[q], w[q], rhs[q], ncell, k, dt);
+    }
   }
   if (rhs_out)
     for (int q = 0; q < NF; ++q) memcpy(rhs_out[q], rhs[q], ncell * sizeof(real));
   for (int k = 0; k < NF; ++k) { free(f[k]); free(w[k]); free(rhs[k]); }
   return 0;
+}
+
+int oracle_integrate(real* const state[NF], int nx, int ny, int nz, int r, const double ds[3],
+                     const oracle_params* p, double dt, int nsteps, int stop_substep,
+                     real* const rhs_out[NF]) {
+  return integrate_form(state, nx, ny, nz, r, ds, p, dt, nsteps, stop_substep, rhs_out, 0);
+}
+/* The same integration with the two-state RK3 form of R#4 (oracle_rk3_update_w2). */
+int oracle_integrate_w2(real* const state[NF], int nx, int ny, int nz, int r, const double ds[3],
+                        const oracle_params* p, double dt, int nsteps, int stop_substep,
+                        real* const rhs_out[NF]) {
+  return integrate_form(state, nx, ny, nz, r, ds, p, dt, nsteps, stop_substep, rhs_out, 1);
 }
 
 /* RHS of an interior state (periodic), without any update: the `debug_rhs` check. */

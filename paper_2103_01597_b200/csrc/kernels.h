@@ -115,6 +115,13 @@ template <typename T, int RAD>
 void launch_zmarch(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
                    const Coef<T>& C, int k, T* rhs_out, int xo, bool persist = false, int zchunk = 0);
 
+// ---- warp-specialised z-marching kernel (zsplit.cuh; FP64, radius 3) ----
+template <typename T, int RAD>
+bool zsplit_supported(const Geom& g, const Region& r);
+template <typename T, int RAD>
+void launch_zsplit(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
+                   const Coef<T>& C, int k, T* rhs_out, int xo, int zchunk = 0);
+
 constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 constexpr int kReduceVals = 5;      // min, max, sum, sum of squares, sum of exp
 

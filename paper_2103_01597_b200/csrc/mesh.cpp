@@ -322,6 +322,7 @@ struct mhd_mesh {
   int cur = 0;
   int next_k = 0;
   int variant = 0;
+  bool split = false;  // variant 0: use the warp-specialised z-march where supported (B2MHD_ZSPLIT)
   int64_t launches = 0;
   double* h_red = nullptr;  // pinned
   TmapSet tmaps[2];          // [state read with the stencil]
@@ -598,9 +599,18 @@ void update_region_r(mhd_mesh* m, cudaStream_t st, const Region& r, int k, doubl
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
   PhaseTimer t(m, st, st == m->stream ? MHD_PHASE_UPDATE : MHD_PHASE_OUTER,
                cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
-  if (zm)
-    launch_zmarch<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, m->persist,
-                          st == m->stream ? 0 : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 0)));
+  const int zchunk = st == m->stream ? 0 : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 0));
+  bool done = false;
+  if constexpr (std::is_same<T, double>::value && RAD == 3) {
+    // warp-specialised variant (zsplit.cuh): variant 3, or variant 0 when enabled for the mesh
+    if (zm && (m->variant == 3 || (m->variant == 0 && m->split)) && zsplit_supported<T, RAD>(m->g, r)) {
+      launch_zsplit<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, zchunk);
+      done = true;
+    }
+  }
+  if (done) {
+  } else if (zm)
+    launch_zmarch<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, m->persist, zchunk);
   else
     launch_direct<T, RAD>(st, in, out, m->g, r, C, k, rhs_out);
   m->launches++;
@@ -1198,6 +1208,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->info = *info;
   if (const char* w = getenv("B2MHD_XWRAP")) m->xwrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_PERSIST")) m->persist_env = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_ZSPLIT")) m->split = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_SLAB_ZCHUNK")) m->slab_zchunk = atoi(w);
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
   if (const char* w = getenv("B2MHD_POISON")) m->debug |= atoi(w) ? MHD_DEBUG_POISON_HALO : 0;
@@ -1490,11 +1501,13 @@ mhd_status mhd_synchronize(mhd_mesh* m) {
 }
 
 mhd_status mhd_set_kernel(mhd_mesh* m, int32_t variant) {
-  if (!m || variant < 0 || variant > 2) return fail(MHD_EINVAL, "variant must be 0, 1 or 2");
-  if (variant == 2) {
+  if (!m || variant < 0 || variant > 3) return fail(MHD_EINVAL, "variant must be 0, 1, 2 or 3");
+  if (variant >= 2) {
     Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
     const bool ok = m->tmaps_ok && (m->info.dtype == MHD_F64 ? zmarch_ok<double>(m, full) : zmarch_ok<float>(m, full));
     if (!ok) return fail(MHD_EUNSUPPORTED, "z-marching kernel does not support this geometry");
+    if (variant == 3 && !(m->info.dtype == MHD_F64 && m->info.radius == 3 && zsplit_supported<double, 3>(m->g, full)))
+      return fail(MHD_EUNSUPPORTED, "the warp-specialised kernel is FP64, radius 3 only");
   }
   m->variant = variant;
   return MHD_OK;

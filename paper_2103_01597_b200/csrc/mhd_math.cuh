@@ -196,22 +196,56 @@ __device__ __forceinline__ MagPart<T> mag_part(const T (&gA)[3][3], const T (&d2
   return m;
 }
 
-// Everything but the magnetic contraction.  u, lnrho, s are the cell values.
+// (B.4) dA/dt = u x B + eta lap A
 template <typename T>
-__device__ __forceinline__ void rhs_rest(T lnrho, T s, const T (&u)[3], const T (&gl)[3], const T (&gs)[3],
-                                         const T (&gu)[3][3], T lapl, T laps, const T (&d2u)[3][3], const T (&xu)[3],
-                                         const MagPart<T>& m, const Coef<T>& C, T out[NF]) {
+__device__ __forceinline__ void rhs_induction(const T (&u)[3], const MagPart<T>& m, const Coef<T>& C, T out[NF]) {
   const T u0 = u[0], u1 = u[1], u2 = u[2];
-  const T divu = (gu[0][0] + gu[1][1]) + gu[2][2];
+  const T B0 = m.B[0], B1 = m.B[1], B2 = m.B[2];
+  out[AX] = fma_(C.eta, m.lapA[0], u1 * B2 - u2 * B1);
+  out[AY] = fma_(C.eta, m.lapA[1], u2 * B0 - u0 * B2);
+  out[AZ] = fma_(C.eta, m.lapA[2], u0 * B1 - u1 * B0);
+}
+
+// Pointwise thermodynamic and magnetic factors of the cell (no derivative of u or s): the
+// equation of state (R#5), the Lorentz acceleration rho^-1 mu0^-1 (mu0 j) x B of B.2 and the ohmic
+// heating of B.3 per unit rho T.  The warp-specialised kernel evaluates these in its magnetic
+// warp group and hands them over; every kernel uses this same split, so results stay bit-identical.
+template <typename T>
+struct Thermo {
+  T L[3];      // (j x B) / rho
+  T ohm;       // (H - C + eta mu0 j^2) / rho
+  T inv_rho;   // 1 / rho
+  T cs2;       // c_s^2
+  T inv_T;     // 1 / T
+};
+
+template <typename T>
+__device__ __forceinline__ Thermo<T> thermo(T lnrho, T s, const MagPart<T>& m, const Coef<T>& C) {
+  Thermo<T> t;
   const T B0 = m.B[0], B1 = m.B[1], B2 = m.B[2];
   const T J0 = m.J[0], J1 = m.J[1], J2 = m.J[2];
-
   // equation of state (R#5): theta = lnT - lnT0
   const T theta = fma_(C.gamma_cp, s, C.gm1 * (lnrho - C.lnrho0));
-  const T inv_rho = exp_(-lnrho);
+  t.inv_rho = exp_(-lnrho);
   const T eth = exp_(theta);
-  const T cs2 = C.cs0sq * eth;
-  const T inv_T = C.inv_T0 / eth;
+  t.cs2 = C.cs0sq * eth;
+  t.inv_T = C.inv_T0 / eth;
+  const T lor = t.inv_rho * C.inv_mu0;
+  t.L[0] = lor * (J1 * B2 - J2 * B1);
+  t.L[1] = lor * (J2 * B0 - J0 * B2);
+  t.L[2] = lor * (J0 * B1 - J1 * B0);
+  const T J2s = fma_(J2, J2, fma_(J1, J1, J0 * J0));
+  t.ohm = fma_(C.eta_inv_mu0, J2s, C.H_C) * t.inv_rho;
+  return t;
+}
+
+// (B.1)-(B.3): lnrho, u, s.  u is the cell value; lapu_i = lap u_i, gdu_i = (grad div u)_i.
+template <typename T>
+__device__ __forceinline__ void rhs_flow(const T (&u)[3], const T (&gl)[3], const T (&gs)[3], const T (&gu)[3][3],
+                                         T lapl, T laps, const T (&lapu)[3], const T (&gdu)[3], const Thermo<T>& t,
+                                         const Coef<T>& C, T out[NF]) {
+  const T u0 = u[0], u1 = u[1], u2 = u[2];
+  const T divu = (gu[0][0] + gu[1][1]) + gu[2][2];
 
   // (B.1) d lnrho/dt = -u.grad lnrho - div u
   out[LNRHO] = -fma_(u2, gl[2], fma_(u1, gl[1], u0 * gl[0])) - divu;
@@ -227,18 +261,14 @@ __device__ __forceinline__ void rhs_rest(T lnrho, T s, const T (&u)[3], const T 
   S[1][2] = S[2][1] = (T)0.5 * (gu[1][2] + gu[2][1]);
 
   // (B.2) momentum
-  const T lor = inv_rho * C.inv_mu0;
-  const T jxB[3] = {J1 * B2 - J2 * B1, J2 * B0 - J0 * B2, J0 * B1 - J1 * B0};
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const T adv = fma_(u2, gu[i][2], fma_(u1, gu[i][1], u0 * gu[i][0]));
     const T pg = fma_(gs[i], C.inv_cp, gl[i]);
-    const T lapu = (d2u[i][0] + d2u[i][1]) + d2u[i][2];
-    const T gdu = d2u[i][i] + xu[i];
     const T sgl = fma_(S[i][2], gl[2], fma_(S[i][1], gl[1], S[i][0] * gl[0]));
     // nu (lap u + 1/3 grad div u + 2 S.grad lnrho) + zeta grad div u
-    const T visc = fma_(C.nu, lapu, fma_(C.two_nu, sgl, fma_(C.nu3, gdu, C.zeta * gdu)));
-    out[UX + i] = fma_(lor, jxB[i], fma_(-cs2, pg, visc - adv));
+    const T visc = fma_(C.nu, lapu[i], fma_(C.two_nu, sgl, fma_(C.nu3, gdu[i], C.zeta * gdu[i])));
+    out[UX + i] = t.L[i] + fma_(-t.cs2, pg, visc - adv);
   }
 
   // (B.3) entropy: -u.grad s + [H - C + eta mu0 j^2]/(rho T) + [2 nu S:S + zeta (div u)^2]/T
@@ -250,21 +280,36 @@ __device__ __forceinline__ void rhs_rest(T lnrho, T s, const T (&u)[3], const T 
   off = fma_(S[0][2], S[0][2], off);
   off = fma_(S[1][2], S[1][2], off);
   SS2 = fma_((T)2, off, SS2);
-  const T J2s = fma_(J2, J2, fma_(J1, J1, J0 * J0));
   const T gth0 = fma_(C.gamma_cp, gs[0], C.gm1 * gl[0]);
   const T gth1 = fma_(C.gamma_cp, gs[1], C.gm1 * gl[1]);
   const T gth2 = fma_(C.gamma_cp, gs[2], C.gm1 * gl[2]);
   const T lapth = fma_(C.gamma_cp, laps, C.gm1 * lapl);
-  const T cond = C.K * inv_rho * fma_(gth2, gth2, fma_(gth1, gth1, fma_(gth0, gth0, lapth)));
-  const T ohm = fma_(C.eta_inv_mu0, J2s, C.H_C) * inv_rho;
+  const T cond = C.K * t.inv_rho * fma_(gth2, gth2, fma_(gth1, gth1, fma_(gth0, gth0, lapth)));
   const T visch = fma_(C.two_nu, SS2, C.zeta * divu * divu);
   const T udgs = fma_(u2, gs[2], fma_(u1, gs[1], u0 * gs[0]));
-  out[SS] = fma_(ohm + visch, inv_T, cond - udgs);
+  out[SS] = fma_(t.ohm + visch, t.inv_T, cond - udgs);
+}
 
-  // (B.4) dA/dt = u x B + eta lap A
-  out[AX] = fma_(C.eta, m.lapA[0], u1 * B2 - u2 * B1);
-  out[AY] = fma_(C.eta, m.lapA[1], u2 * B0 - u0 * B2);
-  out[AZ] = fma_(C.eta, m.lapA[2], u0 * B1 - u1 * B0);
+// The viscous contractions of the u derivatives: lap u_i and (grad div u)_i = d_ii u_i + x_i.
+template <typename T>
+__device__ __forceinline__ void visc_parts(const T (&d2u)[3][3], const T (&xu)[3], T (&lapu)[3], T (&gdu)[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    lapu[i] = (d2u[i][0] + d2u[i][1]) + d2u[i][2];
+    gdu[i] = d2u[i][i] + xu[i];
+  }
+}
+
+// Everything but the magnetic contraction.  u, lnrho, s are the cell values.
+template <typename T>
+__device__ __forceinline__ void rhs_rest(T lnrho, T s, const T (&u)[3], const T (&gl)[3], const T (&gs)[3],
+                                         const T (&gu)[3][3], T lapl, T laps, const T (&d2u)[3][3], const T (&xu)[3],
+                                         const MagPart<T>& m, const Coef<T>& C, T out[NF]) {
+  T lapu[3], gdu[3];
+  visc_parts<T>(d2u, xu, lapu, gdu);
+  const Thermo<T> t = thermo<T>(lnrho, s, m, C);
+  rhs_flow<T>(u, gl, gs, gu, lapl, laps, lapu, gdu, t, C, out);
+  rhs_induction<T>(u, m, C, out);
 }
 
 template <typename T>

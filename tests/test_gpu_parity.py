@@ -5,8 +5,10 @@ Tolerances (BASELINE.json north star):
   * fields after 10 RK3 steps: max relative error <= 1e-11 (FP64), <= 1e-4 (FP32), with the
     per-field floor e = max|g - o| / max(|o|, 1e-3 ||o||_inf) (reading R#18);
   * RHS (debug_rhs): ||g - o||_inf / ||o||_inf <= 1e-12 (FP64), <= 1e-4 (FP32);
-  * increments f(10 steps) - f(0): normwise <= 1e-8 (FP64; the oracle's own double vs
-    long-double floor is ~1e-9 at 12^3, tests/test_oracle_pins.py).
+  * increments f(steps) - f(0): normwise <= 1e-9 against the long-double oracle (FP64; the
+    double oracle's own floor, ~2e-9 at 12^3, tests/test_oracle_pins.py, is not in the way);
+    FP32: <= 2e-2, or the bound FP32 state storage allows where the increment is smaller
+    (_fp32_increment_ok).
 """
 import math
 
@@ -37,6 +39,19 @@ def _field_err(g, o):
 
 def _norm_err(g, o):
     return max(float(np.max(np.abs(g[q] - o[q])) / np.max(np.abs(o[q]))) for q in range(8))
+
+
+def _fp32_increment_ok(got, ref, st, nsub):
+    """FP32 increment parity per field: normwise <= 2e-2, or, where the increment is
+    too small for that, the bound the FP32 state storage itself allows: every substep rounds f to
+    FP32 (|error| <= 2^-24 |f| <= 2^-23 max|f|), so after nsub substeps the increment can be off
+    by nsub 2^-23 max|f| against an exact-arithmetic reference."""
+    for q in range(8):
+        inc_g, inc_o = got[q] - st[q], ref[q] - st[q]
+        den = np.max(np.abs(inc_o))
+        e = float(np.max(np.abs(inc_g - inc_o)) / den)
+        tol = max(2e-2, nsub * 2.0 ** -23 * float(np.max(np.abs(ref[q]))) / den)
+        assert e <= tol, (q, e, tol)
 
 
 # ---- bit-exact data movement --------------------------------------------------------------------
@@ -249,7 +264,9 @@ def test_steps_parity_fp64(n, box, steps):
     got = m.store().cpu().numpy()
     ref = oracle.integrate(st, ds, synth.P0, synth.DT, steps)
     assert _field_err(got, ref) <= 1e-11
-    assert _norm_err(got - st, ref - st) <= 1e-8
+    ref_ld = oracle.integrate(st, ds, synth.P0, synth.DT, steps, kind="ld")
+    inc = (ref_ld - st.astype(np.longdouble)).astype(np.float64)
+    assert _norm_err(got - st, inc) <= 1e-9
     m.close()
 
 
@@ -264,7 +281,30 @@ def test_steps_parity_fp32():
     got = m.store().cpu().numpy().astype(np.float64)
     ref = oracle.integrate(st.astype(np.float64), ds, synth.P0, synth.DT, 10)
     assert _field_err(got, ref) <= 1e-4
+    _fp32_increment_ok(got, ref, st.astype(np.float64), 30)
     m.close()
+
+
+def test_fp32_128_multichunk():
+    """FP32 at 128^3 on one GPU: the 32 x 16 FP32 tile over several 64-plane z chunks, in the
+    launch configuration bench.py --dtype f32 uses; RHS, one RK3 step and its increment against
+    the double oracle fed the FP32-rounded state (R#18)."""
+    import os
+    oracle.set_threads(os.cpu_count() or 1)
+    n = (128, 128, 128)
+    ds = synth.spacing(n)
+    m, _ = _mesh(n, ds, dtype=4)
+    st = synth.splitmix_state((128, 128, 128), (0, 0, 0), (128, 128, 128), dtype=np.float32)
+    st64 = st.astype(np.float64)
+    m.load(st)
+    got_rhs = m.debug_rhs().cpu().numpy().astype(np.float64)
+    assert _norm_err(got_rhs, oracle.rhs(st64, ds, synth.P0)) <= 1e-4
+    m.step(synth.DT)
+    got = m.store().cpu().numpy().astype(np.float64)
+    m.close()
+    ref = oracle.integrate(st64, ds, synth.P0, synth.DT, 1)
+    assert _field_err(got, ref) <= 1e-4
+    _fp32_increment_ok(got, ref, st64, 3)
 
 
 def test_substep_level_parity_and_rk3_order():
@@ -285,23 +325,32 @@ def test_substep_level_parity_and_rk3_order():
 
 
 # ---- kernels agree bit for bit ---------------------------------------------------------------------------
-def test_kernel_variants_bit_identical():
+@pytest.mark.parametrize("n", [(64, 48, 40), (70, 43, 150)])
+def test_kernel_variants_bit_identical(n):
+    """direct (1), z-marching (2) and warp-specialised z-marching (3) kernels: bit-identical RHS
+    and states after two RK3 steps, on a tiled box and on a ragged one with several z chunks"""
     from paper_2103_01597_b200 import MhdError
-    n = (64, 48, 40)
     st = synth.pcg64_state((n[2], n[1], n[0]))
-    outs = []
-    for variant in (1, 2):
+    outs, rhss = [], []
+    for variant in (1, 2, 3):
         m, ds = _mesh(n)
         try:
             m.set_kernel(variant)
         except MhdError:
+            m.close()
+            if variant == 3:
+                continue
             pytest.skip("z-marching kernel not available for this geometry")
         m.load(st)
+        rhss.append(m.debug_rhs().cpu().numpy())
         for _ in range(2):
             m.step(synth.DT)
         outs.append(m.store().cpu().numpy())
         m.close()
-    assert np.array_equal(outs[0], outs[1])
+    assert len(outs) == 3, "warp-specialised kernel unavailable for an FP64 order-6 mesh"
+    for o, r in zip(outs[1:], rhss[1:]):
+        assert np.array_equal(outs[0], o)
+        assert np.array_equal(rhss[0], r)
 
 
 # ---- ABI state machine, reductions --------------------------------------------------------------------
@@ -368,8 +417,9 @@ def test_paper_ulp_analog_256():
     evaluates w in another algebraic form (R#4), so the bar is >= 99.5 % of values within 2 ulps
     in every field and <= 4 ulps everywhere for A (whose increment is small).  Measured on B200:
     A <= 3, lnrho <= 6 ulps; u and s exceed 2 ulps on 0.3 % / 0.2 % of cells, where the large
-    j x B / rho and ohmic-heating increments at 256^3 carry their own rounding
-    (tools/ulp_check.py)."""
+    j x B / rho and ohmic-heating increments at 256^3 cancel against f (tools/ulp_check.py).
+    The binding checks at this size are the north-star ones: fields <= 1e-11 (R#18) and
+    increments <= 1e-9 against the long-double oracle."""
     import os
     oracle.set_threads(os.cpu_count() or 1)
     n = (256, 256, 256)
@@ -381,14 +431,37 @@ def test_paper_ulp_analog_256():
     got = m.store().cpu().numpy()
     m.close()
     ref = oracle.integrate(st, ds, synth.P0, synth.DT, 1)
+    # the north-star tolerances at the benched size (R#18): fields vs the double oracle,
+    # increments vs the long-double oracle
+    assert _field_err(got, ref) <= 1e-11
+    ref_ld = oracle.integrate(st, ds, synth.P0, synth.DT, 1, kind="ld")
+    inc_ld = (ref_ld - st.astype(np.longdouble)).astype(np.float64)
+    del ref_ld
+    assert _norm_err(got - st, inc_ld) <= 1e-9
+    del inc_ld
+    # the same step with the oracle's arithmetic but the two-state RK3 form the GPU stores (R#4)
+    w2 = oracle.integrate(st, ds, synth.P0, synth.DT, 1, form="w2")
+
+    def ulps_of(model, cand):
+        eps = np.exp2(np.floor(np.log2(np.abs(model))) - 52)  # Eq. 15
+        return np.abs(model - cand) / eps                       # Eq. 16
+
     for q in range(8):
         mq, cq = ref[q].ravel(), got[q].ravel()
         assert np.all(mq != 0)
-        eps = np.exp2(np.floor(np.log2(np.abs(mq))) - 52)  # Eq. 15
-        ulps = np.abs(mq - cq) / eps                       # Eq. 16
+        ulps = ulps_of(mq, cq)
         assert np.mean(ulps <= 2.0) >= 0.995, (q, float(np.mean(ulps <= 2.0)))
         if q >= 5:
             assert ulps.max() <= 4.0, (q, float(ulps.max()))
+        # attribution of the > 2-ulp values: they sit where f + dt RHS cancels; the oracle's own
+        # arithmetic, only rearranged into the two-state RK3 form (R#4), misses the 2-ulp bar at
+        # such cells too (measured: u 0.17 %, up to 4.6e4 ulps; s 0.03 %; GPU: u 0.28 %, s 0.19 %,
+        # profiles/r02/ulp_check_w2.json), so the bar is a property of the arrangement of the
+        # arithmetic, not of the GPU path
+        out_gpu = int(np.sum(ulps > 2.0))
+        out_w2 = int(np.sum(ulps_of(mq, w2[q].ravel()) > 2.0))
+        if out_gpu >= 1000:
+            assert out_w2 >= 0.1 * out_gpu, (q, out_gpu, out_w2)
 
 
 # ---- stencil orders 2, 4, 6, 8 -------------------------------------------------------------

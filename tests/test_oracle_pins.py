@@ -449,3 +449,30 @@ def test_double_vs_long_double_oracle_rounding():
         inc_d, inc_ld = d[q] - st[q], ld[q] - st[q]
         # floor: ~30 roundings of f (ulp ~ 1e-16) against an increment of ~5e-6 (lnrho) ~ 1e-9
         assert np.max(np.abs(inc_d - inc_ld)) / np.max(np.abs(inc_ld)) < 2e-9
+
+
+# ---------------------------------------------------------------------------------------------
+# The two-state RK3 form (reading R#4) is the explicit 2N scheme up to rounding
+# ---------------------------------------------------------------------------------------------
+def test_two_state_rk3_form_equals_explicit_form():
+    n = (12, 12, 12)
+    st = pcg64_state(n)
+    ds = (2 * np.pi / 12,) * 3
+    for kind, tol in (("d", 1e-13), ("ld", 1e-15)):  # ld: coefficients rounded to double, as on the GPU
+        w = oracle.integrate(st, ds, P0, 1.19209e-7, 3, kind=kind).astype(np.float64)
+        w2 = oracle.integrate(st, ds, P0, 1.19209e-7, 3, kind=kind, form="w2").astype(np.float64)
+        for q in range(8):
+            e = np.max(np.abs(w[q] - w2[q]) / np.maximum(np.abs(w[q]), 1e-3 * np.max(np.abs(w[q]))))
+            assert e < tol, (kind, q, e)
+    # and on y' = lambda y with a large lambda dt the two forms give the same amplification R(z)
+    lam, dt = -2.0, 0.1
+    z = lam * dt
+    y0 = np.ones((1, 1, 1))
+    st1 = np.zeros((8, 4, 4, 4))
+    st1[0] = 1.0
+    # a uniform state with H = C has RHS = 0 for every field: the state must be a bitwise fixed point
+    p = dict(P0)
+    p["H"] = p["C"] = 0.0
+    fixed = oracle.integrate(st1, (0.5, 0.5, 0.5), p, 0.1, 2, form="w2")
+    assert np.array_equal(fixed, st1)
+    assert abs(float(oracle.rk3_linear(y0, lam, dt, 1)[0, 0, 0]) - (1 + z + z * z / 2 + z ** 3 / 6)) < 1e-15

@@ -48,6 +48,8 @@ def main():
     got = m.store().cpu().numpy()
     m.close()
     ref = oracle.integrate(st, ds, synth.P0, synth.DT, a.steps)
+    # the oracle's arithmetic with the two-state RK3 form the GPU stores (reading R#4)
+    w2 = oracle.integrate(st, ds, synth.P0, synth.DT, a.steps, form="w2")
     out = {"n": a.n, "steps": a.steps, "fields": {}}
     worst = 0.0
     for q, name in enumerate(("lnrho", "ux", "uy", "uz", "ss", "ax", "ay", "az")):
@@ -62,6 +64,17 @@ def main():
         out["fields"][name] = {"max_ulps": float(u.max()), "mean_ulps": float(u.mean()), "hist": hist,
                                "zeros_in_model": int(z.size), "frac_le_2ulps": float(np.mean(u <= 2.0)),
                                "max_ulps_of_max_m_f0": float(u0.max())}
+        # attribution (R#4): the two-state form against the explicit one, and the GPU against it
+        uw, _ = ulp_errors(ref[q], w2[q])
+        ug, _ = ulp_errors(w2[q], got[q])
+        og, ow = u > 2.0, uw > 2.0
+        out["fields"][name].update({
+            "w2_vs_oracle": {"max_ulps": float(uw.max()), "frac_le_2ulps": float(np.mean(uw <= 2.0)),
+                             "n_gt_2": int(ow.sum())},
+            "gpu_vs_w2": {"max_ulps": float(ug.max()), "frac_le_2ulps": float(np.mean(ug <= 2.0)),
+                          "n_gt_2": int((ug > 2.0).sum())},
+            "gpu_outliers": int(og.sum()), "gpu_outliers_also_w2": int((og & ow).sum()),
+            "gpu_outliers_within_2ulps_of_w2": int((og & (ug <= 2.0)).sum())})
         worst = max(worst, float(u.max()))
     out["max_ulps"] = worst
     print(json.dumps(out))
