@@ -52,8 +52,10 @@ def parse():
     ap.add_argument("--order", type=int, choices=(2, 4, 6, 8), default=6,
                     help="stencil order 2r (P:829-830); the paper's benchmarks use 6")
     ap.add_argument("--exchange", choices=("auto", "p2p", "nccl"), default="auto",
-                    help="N > 1: fused peer-memory boundary stores (p2p) or NCCL send/recv of packed segments; "
-                         "auto = p2p at N = 2, 4 (measured faster: DESIGN.md 10), NCCL otherwise")
+                    help="N > 1: boundary results stored into the neighbours' halos over NVLink peer memory "
+                         "(p2p) or NCCL send/recv of packed segments; auto = p2p (measured faster at N = 2, 4: "
+                         "DESIGN.md 10; the 8-rank peer-memory protocol is validated by the one-GPU virtual-rank "
+                         "tests), falling back to NCCL if peer memory cannot be opened on every rank")
     return ap.parse_args()
 
 
@@ -142,10 +144,21 @@ DP_PER_CELL = {2: 368.25, 4: 501.0, 6: 634.25, 8: 768.0}
 NF_BYTES = {"f64": 64, "f32": 32}  # 8 fields x sizeof(T)
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(n_glob, ds, params, dt, seconds_hint=True):
     """The oracle as it stands, on the host cores: one RK3 step (3 substeps) of a periodic slab of
     the bench workload of about 8 M cells (256 x 256 x 128 at 256^3; same cells, same per-cell
-    work; a bounded sample of a few seconds on the host cores)."""
+    work; a bounded sample of a few seconds on the host cores); and the same on ONE core (the
+    paper's CPU model solver was single-core) on a 16-plane slab."""
     import numpy as np
 
     import oracle
@@ -159,9 +172,43 @@ def cpu_baseline(n_glob, ds, params, dt, seconds_hint=True):
     oracle.integrate(st, ds, params, dt, 1)
     el = time.perf_counter() - t0
     cells = nz * n_glob[1] * n_glob[0]
-    return {"value": cells * 3 / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+    oracle.set_threads(1)
+    nz1 = min(16, n_glob[2])
+    t1 = time.perf_counter()
+    oracle.integrate(st[:, :nz1], ds, params, dt, 1)
+    el1 = time.perf_counter() - t1
+    oracle.set_threads(cores)
+    cells1 = nz1 * n_glob[1] * n_glob[0]
+    return {"value": cells * 3 / el / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
             "sample": f"1 RK3 step (3 substeps) of a {n_glob[0]}x{n_glob[1]}x{nz} periodic slab of the "
-                      f"workload, {el:.2f} s wall, OpenMP over z"}
+                      f"workload, {el:.2f} s wall, OpenMP over z",
+            "one_core": {"value": cells1 * 3 / el1 / 1e9, "unit": UNIT, "cores": 1,
+                         "sample": f"1 RK3 step of a {n_glob[0]}x{n_glob[1]}x{nz1} slab, {el1:.2f} s"}}
+
+
+def perf_model(n_glob, world, P_xyz, local_cells, substep_ms, prof, r, cell_bytes):
+    """The paper's model (Eq. 4, tau_0 = 0 as P:406; tools/perfmodel.py) at device level for this
+    run: tau_W = W pi^-1 with pi^-1 the per-cell time of this rank's update kernels (inner +
+    boundary slabs, their device time per substep), tau_Q = Q beta^-1 with Q the remote halo
+    cells of Eq. 7 (both directions) and beta^-1 = bytes per halo cell / NVLink per-direction
+    bandwidth (full duplex).  The driver computes the measured efficiency from the per-N values;
+    efficiency_model is what the model predicts for this N."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import perfmodel
+    P = tuple(reversed(P_xyz))  # Morton coordinate order (z first, reading R#16)
+    n = tuple(reversed(n_glob))
+    upd = prof["update"]["ms"] + prof["outer"]["ms"]
+    nsub = max(prof["update"]["launches"], 1)
+    pi_inv = upd / nsub * 1e-3 / local_cells  # s per cell (device time of the update kernels)
+    link = 770e9  # B200_PROFILING.md peer-copy reference, per direction
+    beta_inv = cell_bytes / link / 2.0
+    q = perfmodel.halo_q(n, P, r, periodic_self=True)
+    tau_w = local_cells * pi_inv
+    tau_q = q * beta_inv
+    return {"equation": "T = max(W pi^-1, Q beta^-1) (Eq. 4, P:331; tau_0 = 0, P:406)", "P": list(P),
+            "pi_inv_ns": pi_inv * 1e9, "beta_inv_ps": beta_inv * 1e12, "remote_halo_cells_Q": q,
+            "tau_w_ms": tau_w * 1e3, "tau_q_ms": tau_q * 1e3, "efficiency_model": tau_w / max(tau_w, tau_q),
+            "substep_ms_measured": substep_ms}
 
 
 def run_reference(args, n_glob, rank):
@@ -194,13 +241,30 @@ def run_reference(args, n_glob, rank):
             "data": "synthetic",
             "config": {"workload": f"{n_glob[0]}^3 FP64 MHD RK3 substep" if n_glob[0] == n_glob[1] == n_glob[2]
                        else f"{n_glob} FP64 MHD RK3 substep", "grid": list(n_glob)},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                              "sample": f"per step: 1 substep of a {n_glob[0]}x{n_glob[1]}x{nz} periodic slab"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line, on the real stdout (everything else, e.g. the NCCL version banner some
+    environments print at communicator creation, goes to stderr)."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
+    # keep stdout for the JSON line alone: fd 1 is pointed at stderr for the libraries
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -242,9 +306,29 @@ def main():
     dtype = b2.MHD_F64 if args.dtype == "f64" else b2.MHD_F32
     es = 8 if dtype == b2.MHD_F64 else 4
     ds = synth.spacing(n_glob)
-    exchange = args.exchange if args.exchange != "auto" else ("p2p" if world in (2, 4) else "nccl")
-    mesh = b2.Mesh(n_glob, ds, synth.P0, dtype, rank=rank, nranks=world, exchange_corners=args.corners,
-                   kernel=args.kernel, exchange=exchange, radius=args.order // 2)
+    exchange = args.exchange if args.exchange != "auto" else "p2p"
+
+    def make_mesh(ex):
+        return b2.Mesh(n_glob, ds, synth.P0, dtype, rank=rank, nranks=world, exchange_corners=args.corners,
+                       kernel=args.kernel, exchange=ex, radius=args.order // 2)
+
+    if world > 1 and args.exchange == "auto":
+        # peer memory on every rank, else NCCL everywhere (the ranks must agree)
+        mesh, err = None, None
+        try:
+            mesh = make_mesh("p2p")
+        except Exception as e:  # pragma: no cover - hardware dependent
+            err = e
+        ok = torch.tensor([0 if mesh is None else 1], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            if mesh is not None:
+                mesh.close()
+            if rank == 0:
+                print(f"bench: peer-memory exchange unavailable ({err}); using NCCL", file=sys.stderr)
+            mesh = make_mesh("nccl")
+    else:
+        mesh = make_mesh(exchange)
     nz, ny, nx = mesh.shape
     lo = tuple(c * n for c, n in zip(reversed(mesh.coord), (nz, ny, nx)))
     npdt = np.float64 if dtype == b2.MHD_F64 else np.float32
@@ -382,6 +466,21 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if world > 1:
+            # several ranks: the inner launch and the boundary slabs (side stream) run concurrently,
+            # so the roofline counts every cell this rank updates over the whole device-timed
+            # substep (inner + outer + exchange): a lower bound on the kernels' own rate
+            sub_s = substep_ms * 1e-3
+            line["roofline_substep"] = {
+                "bound": "alu" if dp_per_cell else "hbm",
+                "achieved": (dp_per_cell * local_cells / sub_s) if dp_per_cell else
+                            (NF_BYTES[args.dtype] * (2 + 3 + 3) / 3 * local_cells / sub_s / 1e9),
+                "peak": FP64_PEAK_LANE_OPS if dp_per_cell else hbm_peak,
+                "unit": "DP lane-ops/s" if dp_per_cell else "GB/s",
+                "scope": "all update kernels of one rank (inner + boundary slabs) over the device-timed substep"}
+            line["roofline_substep"]["frac"] = line["roofline_substep"]["achieved"] / line["roofline_substep"]["peak"]
+            line["model"] = perf_model(n_glob, world, P, local_cells, substep_ms, prof, args.order // 2,
+                                       NF_BYTES[args.dtype])
         if dp_per_cell and up["ms"] > 0:
             # FP64: the kernel is bound by on-chip work (FP64 pipe and shared-memory wavefronts,
             # DESIGN.md 7), not by HBM, so the FP64 roof is the primary one and HBM secondary.
@@ -394,7 +493,7 @@ def main():
                                 "kernel": roofline["kernel"], "avg_launch_ms": upd_ms,
                                 "peak_source": "measured DFMA microbenchmark, 17.09e12 lane-ops/s = 92 % of "
                                                "148 SM x 64 FP64 lanes x 1.965 GHz (profiles/r01_fp64_lds_microbench.txt)"}
-        print(json.dumps(line), flush=True)
+        emit(line)
     mesh.close()
     if dist is not None:
         dist.destroy_process_group()

@@ -323,6 +323,9 @@ struct mhd_mesh {
   int next_k = 0;
   int variant = 0;
   bool split = false;  // variant 0: use the warp-specialised z-march where supported (B2MHD_ZSPLIT)
+  // peer-memory substeps: each boundary slab waits only for the neighbours whose halo it reads
+  // (B2MHD_FINE_ARRIVAL=0: one wait for every neighbour before the first slab, the round-1 schedule)
+  bool fine_arrival = true;
   int64_t launches = 0;
   double* h_red = nullptr;  // pinned
   TmapSet tmaps[2];          // [state read with the stencil]
@@ -579,6 +582,41 @@ void xr_done(mhd_mesh* m, cudaStream_t st, unsigned long long s) {
     m->launches++;
   }
 }
+// Fine-grained arrival (mhd_mesh::fine_arrival): the three parts of xr_arrive + xr_wait separately.
+// xr_signal_arrive(s): publish arrive = s (all earlier work of this rank is complete: it is done
+// reading the halo the neighbours are about to overwrite), without waiting.
+void xr_signal_arrive(mhd_mesh* m, cudaStream_t st, unsigned long long s) {
+  if (m->group) {
+    cudaEventRecord(m->ev_arrive[s % kRing], st);
+  } else {
+    launch_p2p_signal(st, m->peer_arrive, s);
+    m->launches++;
+  }
+}
+// wait for done >= s of the neighbours `which` (indices into m->peers)
+void xr_wait_done_of(mhd_mesh* m, cudaStream_t st, unsigned long long s, const std::vector<int>& which) {
+  if (s == 0 || which.empty()) return;
+  if (m->group) {
+    for (int i : which) cudaStreamWaitEvent(st, m->group->m[m->peers[i].peer]->ev_done[s % kRing], 0);
+  } else {
+    FlagSet fs;
+    memset(&fs, 0, sizeof(fs));
+    for (int i : which) fs.ptr[fs.n++] = m->my_done.ptr[i];
+    launch_p2p_wait(st, fs, s, m->err_word(), m->spin_timeout_ns);
+    m->launches++;
+  }
+}
+// wait for arrive >= s of every neighbour
+void xr_wait_arrive(mhd_mesh* m, cudaStream_t st, unsigned long long s) {
+  if (m->peers.empty()) return;
+  if (m->group) {
+    for (auto& p : m->peers) cudaStreamWaitEvent(st, m->group->m[p.peer]->ev_arrive[s % kRing], 0);
+  } else {
+    launch_p2p_wait(st, m->my_arrive, s, m->err_word(), m->spin_timeout_ns);
+    m->launches++;
+  }
+}
+
 // wait until every neighbour finished operation s (its stores into this rank's halo have landed)
 void xr_wait_done(mhd_mesh* m, cudaStream_t st, unsigned long long s) {
   if (s == 0 || m->peers.empty()) return;
@@ -698,6 +736,28 @@ void split_regions(const mhd_mesh* m, Region& inner, std::vector<Region>& outer,
   if (inner.ext[0] <= 0 || inner.ext[1] <= 0 || inner.ext[2] <= 0) inner.ext[0] = inner.ext[1] = inner.ext[2] = 0;
 }
 
+// The neighbours (indices into m->peers) whose halo cells the stencil of region r reads: every
+// remote P:705 segment whose halo box meets r grown by the radius; 3-D corner segments are never
+// read (Eq. 14 has no 3-D corner points).
+std::vector<int> region_peers(const mhd_mesh* m, const Region& r) {
+  std::vector<int> out;
+  const int rad = m->info.radius;
+  for (auto& si : m->segs) {
+    if (si.self || si.s.kind == 3) continue;
+    bool meets = true;
+    for (int a = 0; a < 3; ++a) {
+      const int h0 = si.s.dst_first[a], h1 = h0 + si.s.extent[a];
+      const int b0 = r.lo[a] - rad, b1 = r.lo[a] + r.ext[a] + rad;
+      meets = meets && h0 < b1 && b0 < h1;
+    }
+    if (!meets) continue;
+    for (size_t i = 0; i < m->peers.size(); ++i)
+      if (m->peers[i].peer == si.s.recv_peer && std::find(out.begin(), out.end(), (int)i) == out.end())
+        out.push_back((int)i);
+  }
+  return out;
+}
+
 // Boundary-slab widths (x, y, z): one tile wide in x and y so that the slabs run on the tiled
 // kernel; in z 8 planes for the packed exchange (the slabs wait for it: keep them small) and 16
 // for the peer-memory exchange (the slabs run first, beside the inner segment: fewer planes lost
@@ -759,7 +819,10 @@ mhd_status op_p2p_substep(mhd_mesh* m, int ph, int k, double dt, T* rhs_out) {
     CU(cudaEventRecord(m->ev_ready, m->stream));
     CU(cudaStreamWaitEvent(m->comm_stream, m->ev_ready, 0));
     PhaseTimer t(m, m->comm_stream, MHD_PHASE_EXCHANGE, 0.0);
-    xr_arrive(m, m->comm_stream, m->op_seq);
+    if (m->fine_arrival)
+      xr_signal_arrive(m, m->comm_stream, m->op_seq);
+    else
+      xr_arrive(m, m->comm_stream, m->op_seq);
     CU(cudaGetLastError());
     return MHD_OK;
   }
@@ -769,9 +832,16 @@ mhd_status op_p2p_substep(mhd_mesh* m, int ph, int k, double dt, T* rhs_out) {
   int thick[3];
   slab_thickness<T>(m, thick);
   split_regions(m, inner, outer, thick);
-  xr_wait(m, m->comm_stream, s);
+  if (!m->fine_arrival) xr_wait(m, m->comm_stream, s);
   m->g.xwrap = !rhs_out && xw ? 1 : 0;
-  for (auto& r : outer) update_region<T>(m, r, k, dt, rhs_out, m->comm_stream);
+  for (auto& r : outer) {
+    // per-slab arrival (the fine-grained start of P:1013): this slab waits only
+    // until the neighbours whose halo it reads have landed their stores of operation s - 1
+    if (m->fine_arrival) xr_wait_done_of(m, m->comm_stream, s - 1, region_peers(m, r));
+    update_region<T>(m, r, k, dt, rhs_out, m->comm_stream);
+  }
+  // the copy into the neighbours' halos of the new state waits until each is done reading it
+  if (m->fine_arrival) xr_wait_arrive(m, m->comm_stream, s);
   if (!rhs_out) {
     PhaseTimer t(m, m->comm_stream, MHD_PHASE_PACK, seg_bytes(m->remote_list, sizeof(T)));
     launch_remote_copy<T>(m->comm_stream, m->fields<T>(1 - m->cur), m->g, m->remote_list, m->remote_map<T>(1 - m->cur));
@@ -1209,6 +1279,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   if (const char* w = getenv("B2MHD_XWRAP")) m->xwrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_PERSIST")) m->persist_env = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_ZSPLIT")) m->split = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_FINE_ARRIVAL")) m->fine_arrival = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_SLAB_ZCHUNK")) m->slab_zchunk = atoi(w);
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
   if (const char* w = getenv("B2MHD_POISON")) m->debug |= atoi(w) ? MHD_DEBUG_POISON_HALO : 0;

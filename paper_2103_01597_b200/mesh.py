@@ -52,7 +52,19 @@ class Mesh:
             if exchange == "p2p":
                 blobs = [None] * nranks
                 dist.all_gather_object(blobs, native.mhd_p2p_export(self.handle), group=process_group)
-                native.mhd_p2p_open(self.handle, blobs)
+                err = None
+                try:
+                    native.mhd_p2p_open(self.handle, blobs)
+                except native.MhdError as e:
+                    err = e
+                # every rank learns whether every rank opened its neighbours' memory, so that a
+                # failure raises everywhere (no rank is left waiting in a collective)
+                flag = torch.tensor([0 if err else 1], dtype=torch.int32, device=self.device)
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=process_group)
+                if not int(flag.item()):
+                    native.mhd_mesh_destroy(self.handle)
+                    self.handle = None
+                    raise RuntimeError(f"peer-memory exchange unavailable on some rank ({err or 'remote'})")
                 dist.barrier(group=process_group)
                 self._barrier_on_close = True
             elif exchange != "nccl":
