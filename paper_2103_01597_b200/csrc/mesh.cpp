@@ -317,6 +317,7 @@ struct mhd_mesh {
   // 65.3 -> 82.7 Gcell/s at 4 GPUs), the default 64 for FP64 (16: -2 %; profiles/r01/bench_szc*).
   // B2MHD_SLAB_ZCHUNK=n overrides (0: 64).
   int slab_zchunk = -1;
+  int zchunk_env = -1;  // z chunk of main-stream update launches (-1: wave-balanced, zmarch.cuh)
   int slab_env[3] = {0, 0, 0};
   ncclComm_t comm = nullptr;
   int cur = 0;
@@ -637,7 +638,9 @@ void update_region_r(mhd_mesh* m, cudaStream_t st, const Region& r, int k, doubl
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
   PhaseTimer t(m, st, st == m->stream ? MHD_PHASE_UPDATE : MHD_PHASE_OUTER,
                cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
-  const int zchunk = st == m->stream ? 0 : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 0));
+  // main stream: wave-balanced z chunks (B2MHD_ZCHUNK overrides); boundary slabs: 16 (FP32) / 64
+  const int zchunk = st == m->stream ? m->zchunk_env
+                                     : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 0));
   bool done = false;
   if constexpr (std::is_same<T, double>::value && RAD == 3) {
     // warp-specialised variant (zsplit.cuh): variant 3, or variant 0 when enabled for the mesh
@@ -1281,6 +1284,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   if (const char* w = getenv("B2MHD_ZSPLIT")) m->split = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_FINE_ARRIVAL")) m->fine_arrival = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_SLAB_ZCHUNK")) m->slab_zchunk = atoi(w);
+  if (const char* w = getenv("B2MHD_ZCHUNK")) m->zchunk_env = atoi(w);
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
   if (const char* w = getenv("B2MHD_POISON")) m->debug |= atoi(w) ? MHD_DEBUG_POISON_HALO : 0;
   if (const char* w = getenv("B2MHD_SPIN_TIMEOUT_S")) m->spin_timeout_ns = (unsigned long long)(atof(w) * 1e9);

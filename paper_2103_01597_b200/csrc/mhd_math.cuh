@@ -52,6 +52,36 @@ template <typename T> __device__ __forceinline__ T exp_(T x);
 template <> __device__ __forceinline__ double exp_<double>(double x) { return exp(x); }
 template <> __device__ __forceinline__ float exp_<float>(float x) { return expf(x); }
 
+#ifdef __CUDACC__
+// Two FP32 cells evaluated together (the FP32 z-marching kernel gives each thread two cells of a
+// column): every arithmetic operation is one sm_100a FP32x2 instruction (FFMA2 / FADD2 / FMUL2)
+// whose lanes round exactly as the scalar FP32 instruction, so each lane's result is bit-identical
+// to the scalar kernels' (R#19).
+struct alignas(8) F2 {
+  float2 v;
+  F2() = default;
+  __host__ __device__ explicit F2(double c) : v(make_float2((float)c, (float)c)) {}
+  __host__ __device__ F2(float a, float b) : v(make_float2(a, b)) {}
+};
+__device__ __forceinline__ F2 mk2(float2 a) {
+  F2 r;
+  r.v = a;
+  return r;
+}
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return mk2(__fadd2_rn(a.v, b.v)); }
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return mk2(__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))); }
+// The product is an FFMA2 with an addend of -0 that the compiler cannot see (b2_f2_nz, set to
+// (-0, -0) by the launcher; a*b + -0 == a*b exactly): the CUDA 12.9 compiler contracts an FP32x2
+// multiply followed by an add into FFMA2 even with -fmad=false and explicit .rn (also at the PTX
+// level), which would round differently from the scalar kernels.
+static __constant__ float2 b2_f2_nz;
+__device__ __forceinline__ F2 operator*(F2 a, F2 b) { return mk2(__ffma2_rn(a.v, b.v, b2_f2_nz)); }
+__device__ __forceinline__ F2 operator/(F2 a, F2 b) { return F2(a.v.x / b.v.x, a.v.y / b.v.y); }
+__device__ __forceinline__ F2 operator-(F2 a) { return F2(-a.v.x, -a.v.y); }
+template <> __device__ __forceinline__ F2 fma_<F2>(F2 a, F2 b, F2 c) { return mk2(__ffma2_rn(a.v, b.v, c.v)); }
+template <> __device__ __forceinline__ F2 exp_<F2>(F2 x) { return F2(expf(x.v.x), expf(x.v.y)); }
+#endif
+
 // ---- canonical operator forms -------------------------------------------------------------
 // D1 along an axis from the differences  Dl_i = f(+i) - f(-i), i = 1..RAD
 template <typename T, int RAD>

@@ -69,6 +69,18 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
+#ifndef B2_ZM_F32_CPT
+#define B2_ZM_F32_CPT 1
+#endif
+template <int CPT, typename T>
+struct ZVal {
+  using type = T;
+};
+template <>
+struct ZVal<2, float> {
+  using type = F2;
+};
+
 template <typename T, int RAD>
 struct ZCfg {
   static constexpr int TX = zm_tx<T>(), TY = zm_ty<T, RAD>();
@@ -80,7 +92,14 @@ struct ZCfg {
   // r + 2 slots: planes o..o+r in use while o+r+1 streams in.  One CTA per SM (a 16x8 FP64 tile at
   // two CTAs per SM and a 2-CTA FP32 variant both measured slower: profiles/r01/).
   static constexpr int NSLOT = RAD + 2;
-  static constexpr int NT = TX * TY;
+  // cells per thread.  B2_ZM_F32_CPT=2 (build option): FP32 threads own two cells of a column
+  // (rows y and y + RS of the tile) and evaluate both with FP32x2 instructions (FFMA2 / FADD2,
+  // mhd_math.cuh::F2), bit-identical to the scalar kernels; -31 % instructions, but at 246
+  // registers only 8 warps fit and the kernel is latency bound: 22.8 vs 24.6 Gcell/s at 256^3
+  // (profiles/r02/f32_*), so the default is one cell per thread (16 warps)
+  static constexpr int CPT = sizeof(T) == 4 && RAD <= 3 ? B2_ZM_F32_CPT : 1;
+  static constexpr int RS = TY / CPT;
+  static constexpr int NT = TX * TY / CPT;
   static constexpr int CH = zm_ch<T>();
   static constexpr int PCOLS = zm_pcols<T>();
   static constexpr int PSZ = (TY * PCOLS * ES + 127) / 128 * 128 / ES;  // f_{k-1} tile per field
@@ -89,7 +108,17 @@ struct ZCfg {
   static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128 + 16;
   static constexpr bool FITS = SMEM <= 227 * 1024;
   static constexpr bool SKEW = TY < 8;  // the 4-row tiles (FP64, r = 4)
+  using V = typename ZVal<CPT, T>::type;  // compute type: T, or two FP32 cells (F2)
 };
+
+// lane c of a compute value (the cell in row y + c RS of a two-cell FP32 thread)
+template <typename V>
+__device__ __forceinline__ auto lane_of(V v, int c) {
+  if constexpr (std::is_same<V, F2>::value)
+    return c == 0 ? v.v.x : v.v.y;
+  else
+    return v;
+}
 
 // Register state carried along z by one thread.
 template <typename T, int RAD>
@@ -101,9 +130,10 @@ struct March {
 template <typename T, int RAD, int MODE>
 struct ZStep {
   using Z = ZCfg<T, RAD>;
+  using V = typename Z::V;  // compute type (storage type T)
   const T* ring;
   const T* prevbuf;
-  const Coef<T>& C;
+  const Coef<V>& C;
   int cell;   // offset of this thread's cell inside a field of a slot
   int pcell;  // offset inside a field of the f_{k-1} tile
   int slot0;  // plane zb - r (first staged plane) has slot 0
@@ -116,45 +146,56 @@ struct ZStep {
   __device__ __forceinline__ const T* slot_of(int plane) const {
     return ring + ((plane - slot0) % Z::NSLOT) * Z::SLOT + cell;
   }
-  static __device__ __forceinline__ T at(const T* sp, int q, int dx, int dy) {
-    return sp[q * Z::FSZ + dy * Z::COLS + dx];
+  // field q at offset (dx, dy) in a staged plane: this thread's cell, or its two cells (rows y, y + RS)
+  static __device__ __forceinline__ V at(const T* sp, int q, int dx, int dy) {
+    const T* e = sp + q * Z::FSZ + dy * Z::COLS + dx;
+    if constexpr (Z::CPT == 2)
+      return V(e[0], e[Z::RS * Z::COLS]);
+    else
+      return e[0];
+  }
+  static __device__ __forceinline__ V at_prev(const T* pv) {
+    if constexpr (Z::CPT == 2)
+      return V(pv[0], pv[Z::RS * Z::PCOLS]);
+    else
+      return pv[0];
   }
 
   // x/y first and second derivatives of field q in the slot, with the differences kept
-  __device__ __forceinline__ void axis_xy(const T* sp, int q, T f0, T (&d1)[2], T (&d2)[2], T (&dlx)[RAD],
-                                          T (&dly)[RAD]) const {
-    T sgx[RAD], sgy[RAD];
+  __device__ __forceinline__ void axis_xy(const T* sp, int q, V f0, V (&d1)[2], V (&d2)[2], V (&dlx)[RAD],
+                                          V (&dly)[RAD]) const {
+    V sgx[RAD], sgy[RAD];
 #pragma unroll
     for (int i = 1; i <= RAD; ++i) {
-      const T px = at(sp, q, i, 0), mx = at(sp, q, -i, 0);
-      const T py = at(sp, q, 0, i), my = at(sp, q, 0, -i);
+      const V px = at(sp, q, i, 0), mx = at(sp, q, -i, 0);
+      const V py = at(sp, q, 0, i), my = at(sp, q, 0, -i);
       dlx[i - 1] = px - mx;
       sgx[i - 1] = px + mx;
       dly[i - 1] = py - my;
       sgy[i - 1] = py + my;
     }
-    d1[0] = d1_of<T, RAD>(dlx, C.c1[0]);
-    d2[0] = d2_of<T, RAD>(f0, sgx, C.d2[0], C.d0[0]);
-    d1[1] = d1_of<T, RAD>(dly, C.c1[1]);
-    d2[1] = d2_of<T, RAD>(f0, sgy, C.d2[1], C.d0[1]);
+    d1[0] = d1_of<V, RAD>(dlx, C.c1[0]);
+    d2[0] = d2_of<V, RAD>(f0, sgx, C.d2[0], C.d0[0]);
+    d1[1] = d1_of<V, RAD>(dly, C.c1[1]);
+    d2[1] = d2_of<V, RAD>(f0, sgy, C.d2[1], C.d0[1]);
   }
   // z derivatives from the column: f(o+1..o+r) from the ring, f(o-r..o-1) from registers
   template <int PH>
-  __device__ __forceinline__ void axis_z(const March<T, RAD>& st, int q, T f0, const T* const (&sk)[RAD + 1], T& d1,
-                                         T& d2) const {
-    T dl[RAD], sg[RAD];
+  __device__ __forceinline__ void axis_z(const March<V, RAD>& st, int q, V f0, const T* const (&sk)[RAD + 1], V& d1,
+                                         V& d2) const {
+    V dl[RAD], sg[RAD];
 #pragma unroll
     for (int i = 1; i <= RAD; ++i) {
-      const T p = at(sk[i], q, 0, 0), m = st.hist[q][(RAD - i + PH) % RAD];
+      const V p = at(sk[i], q, 0, 0), m = st.hist[q][(RAD - i + PH) % RAD];
       dl[i - 1] = p - m;
       sg[i - 1] = p + m;
     }
-    d1 = d1_of<T, RAD>(dl, C.c1[2]);
-    d2 = d2_of<T, RAD>(f0, sg, C.d2[2], C.d0[2]);
+    d1 = d1_of<V, RAD>(dl, C.c1[2]);
+    d2 = d2_of<V, RAD>(f0, sg, C.d2[2], C.d0[2]);
   }
-  __device__ __forceinline__ T cross_xy_s(const T* sp, int q) const {
-    const T* w = C.xw[0];
-    T a = (-w[RAD - 1]) * (at(sp, q, RAD, -RAD) - at(sp, q, -RAD, -RAD));
+  __device__ __forceinline__ V cross_xy_s(const T* sp, int q) const {
+    const V* w = C.xw[0];
+    V a = (-w[RAD - 1]) * (at(sp, q, RAD, -RAD) - at(sp, q, -RAD, -RAD));
 #pragma unroll
     for (int k = -RAD + 1; k <= RAD; ++k) {
       if (k == 0) continue;
@@ -166,19 +207,19 @@ struct ZStep {
   // k < 0 half of the z-cross terms of plane p for vector v: outputs p+j (k = -j, j < r) and a
   // fresh accumulator for p+r (k = -r), which lands in the physical slot of output p.
   template <int PH>
-  __device__ __forceinline__ void push(March<T, RAD>& st, int v, const T (&dlx_x)[RAD], const T (&dly_y)[RAD],
-                                       const T (&dlx_z)[RAD], const T (&dly_z)[RAD]) const {
-    const T* wxz = C.xw[1];
-    const T* wyz = C.xw[2];
+  __device__ __forceinline__ void push(March<V, RAD>& st, int v, const V (&dlx_x)[RAD], const V (&dly_y)[RAD],
+                                       const V (&dlx_z)[RAD], const V (&dly_z)[RAD]) const {
+    const V* wxz = C.xw[1];
+    const V* wyz = C.xw[2];
 #pragma unroll
     for (int j = 1; j < RAD; ++j) {
-      T* a = st.acc[v][(j + PH) % RAD];
+      V* a = st.acc[v][(j + PH) % RAD];
       a[0] = fma_(-wxz[j - 1], dlx_z[j - 1], a[0]);
       a[1] = fma_(-wyz[j - 1], dly_z[j - 1], a[1]);
       a[2] = fma_(-wxz[j - 1], dlx_x[j - 1], a[2]);
       a[2] = fma_(-wyz[j - 1], dly_y[j - 1], a[2]);
     }
-    T* f = st.acc[v][(0 + PH) % RAD];
+    V* f = st.acc[v][(0 + PH) % RAD];
     f[0] = (-wxz[RAD - 1]) * dlx_z[RAD - 1];
     f[1] = (-wyz[RAD - 1]) * dly_z[RAD - 1];
     f[2] = fma_(-wyz[RAD - 1], dly_y[RAD - 1], (-wxz[RAD - 1]) * dlx_x[RAD - 1]);
@@ -186,12 +227,12 @@ struct ZStep {
 
   // push-only pass over a plane below the chunk (prologue)
   template <int PH>
-  __device__ __forceinline__ void push_only(March<T, RAD>& st, int p) const {
+  __device__ __forceinline__ void push_only(March<V, RAD>& st, int p) const {
     const T* s0 = slot_of(p);
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       const int qx = v == 0 ? UX : AX;
-      T dlx_x[RAD], dly_y[RAD], dlx_z[RAD], dly_z[RAD];
+      V dlx_x[RAD], dly_y[RAD], dlx_z[RAD], dly_z[RAD];
 #pragma unroll
       for (int i = 1; i <= RAD; ++i) {
         dlx_x[i - 1] = at(s0, qx, i, 0) - at(s0, qx, -i, 0);
@@ -209,15 +250,15 @@ struct ZStep {
   // Derivatives of one vector field (u or A) at output plane o: first and second derivatives
   // along every axis, the graddiv cross parts, and the push of plane o's differences.
   template <int PH>
-  __device__ __forceinline__ void vector_derivs(March<T, RAD>& st, int v, const T* const (&sk)[RAD + 1], T (&f)[3],
-                                                T (&g)[3][3], T (&d2)[3][3], T (&x)[3]) const {
+  __device__ __forceinline__ void vector_derivs(March<V, RAD>& st, int v, const T* const (&sk)[RAD + 1], V (&f)[3],
+                                                V (&g)[3][3], V (&d2)[3][3], V (&x)[3]) const {
     const int qx = v == 0 ? UX : AX;
     const T* s0 = sk[0];
-    T dlx[3][RAD], dly[3][RAD];
+    V dlx[3][RAD], dly[3][RAD];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const int q = qx + c;
-      T d1a[2], d2a[2];
+      V d1a[2], d2a[2];
       f[c] = at(s0, q, 0, 0);
       axis_xy(s0, q, f[c], d1a, d2a, dlx[c], dly[c]);
       axis_z<PH>(st, q, f[c], sk, g[c][2], d2[c][2]);
@@ -227,14 +268,14 @@ struct ZStep {
       d2[c][1] = d2a[1];
     }
     // graddiv cross parts: k < 0 (accumulated), + in-plane part at k = 0, then k = 1..r
-    const T P0 = cross_xy_s(s0, qx + 1);  // d_x d_y v_y
-    const T P1 = cross_xy_s(s0, qx);      // d_x d_y v_x
-    const T* a = st.acc[v][(0 + PH) % RAD];
+    const V P0 = cross_xy_s(s0, qx + 1);  // d_x d_y v_y
+    const V P1 = cross_xy_s(s0, qx);      // d_x d_y v_x
+    const V* a = st.acc[v][(0 + PH) % RAD];
     x[0] = a[0] + P0;
     x[1] = a[1] + P1;
     x[2] = a[2];
-    const T* wxz = C.xw[1];
-    const T* wyz = C.xw[2];
+    const V* wxz = C.xw[1];
+    const V* wyz = C.xw[2];
 #pragma unroll
     for (int kk = 1; kk <= RAD; ++kk) {
       const T* s = sk[kk];
@@ -247,25 +288,25 @@ struct ZStep {
   }
 
   template <int PH>
-  __device__ __forceinline__ void full(March<T, RAD>& st, int o, const Fields<T>& out, const Geom& g, int k,
-                                       bool active, int x, int y, T* rhs_out) const {
+  __device__ __forceinline__ void full(March<V, RAD>& st, int o, const Fields<T>& out, const Geom& g, int k,
+                                       const bool (&active)[Z::CPT], int x, int y, T* rhs_out) const {
     const T* sk[RAD + 1];
 #pragma unroll
     for (int i = 0; i <= RAD; ++i) sk[i] = slot_of(o + i);
     // magnetic potential: derivatives, then B, mu0 j, lap A right away
-    T fA[3], gA[3][3], d2A[3][3], xA[3];
+    V fA[3], gA[3][3], d2A[3][3], xA[3];
     vector_derivs<PH>(st, 1, sk, fA, gA, d2A, xA);
-    const MagPart<T> m = mag_part<T>(gA, d2A, xA);
+    const MagPart<V> m = mag_part<V>(gA, d2A, xA);
     // velocity
-    T u[3], gu[3][3], d2u[3][3], xu[3];
+    V u[3], gu[3][3], d2u[3][3], xu[3];
     vector_derivs<PH>(st, 0, sk, u, gu, d2u, xu);
     signal_half(o);
     // log density and entropy
-    T sc[2], gsc[2][3], lap[2];
+    V sc[2], gsc[2][3], lap[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int q = h == 0 ? LNRHO : SS;
-      T d1a[2], d2a[2], dlx[RAD], dly[RAD], d2z;
+      V d1a[2], d2a[2], dlx[RAD], dly[RAD], d2z;
       sc[h] = at(sk[0], q, 0, 0);
       axis_xy(sk[0], q, sc[h], d1a, d2a, dlx, dly);
       axis_z<PH>(st, q, sc[h], sk, gsc[h][2], d2z);
@@ -273,36 +314,42 @@ struct ZStep {
       gsc[h][1] = d1a[1];
       lap[h] = (d2a[0] + d2a[1]) + d2z;
     }
-    T rhs[NF];
-    rhs_rest<T>(sc[0], sc[1], u, gsc[0], gsc[1], gu, lap[0], lap[1], d2u, xu, m, C, rhs);
-    const T fk[NF] = {sc[0], u[0], u[1], u[2], sc[1], fA[0], fA[1], fA[2]};
-    if (active) {
-      const long long gidx = (long long)o * g.sz + (long long)y * g.sy + x;
+    V rhs[NF];
+    rhs_rest<V>(sc[0], sc[1], u, gsc[0], gsc[1], gu, lap[0], lap[1], d2u, xu, m, C, rhs);
+    const V fk[NF] = {sc[0], u[0], u[1], u[2], sc[1], fA[0], fA[1], fA[2]};
+    if (active[0] || (Z::CPT == 2 && active[Z::CPT - 1])) {
+      V fn[NF];
       if (MODE == 0) {
         const T* pv = prevbuf + ((o & 1) * NF) * Z::PSZ + pcell;
-        T fn[NF];
 #pragma unroll
-        for (int q = 0; q < NF; ++q) {
-          fn[q] = rk_update<T>(k, fk[q], k > 0 ? pv[q * Z::PSZ] : (T)0, rhs[q], C);
-          out.f[q][gidx] = fn[q];
-        }
-        if (g.xwrap) {
-          // periodic x faces of this rank's own halo (x unsplit) written here: the cells in
-          // the first / last 32-byte sector of a row also go to the row padding on the other side
-          // (whole sectors: the extra cell lands in unused padding).  (Adding the y faces here
-          // pushed the kernel to 255 registers with spills: the y rows are copied instead.)
-          constexpr int W = 32 / (int)sizeof(T);
-          const long long sh = x < W ? (long long)g.nx : (x >= g.nx - W ? -(long long)g.nx : 0);
-          if (sh != 0) {
+        for (int q = 0; q < NF; ++q) fn[q] = rk_update<V>(k, fk[q], k > 0 ? at_prev(pv + q * Z::PSZ) : (V)0, rhs[q], C);
+      }
 #pragma unroll
-            for (int q = 0; q < NF; ++q) out.f[q][gidx + sh] = fn[q];
+      for (int c = 0; c < Z::CPT; ++c) {
+        if (!active[c]) continue;
+        const int yc = y + c * Z::RS;
+        const long long gidx = (long long)o * g.sz + (long long)yc * g.sy + x;
+        if (MODE == 0) {
+#pragma unroll
+          for (int q = 0; q < NF; ++q) out.f[q][gidx] = lane_of(fn[q], c);
+          if (g.xwrap) {
+            // periodic x faces of this rank's own halo (x unsplit) written here: the cells
+            // in the first / last 32-byte sector of a row also go to the row padding on the other
+            // side (whole sectors: the extra cell lands in unused padding).  (Adding the y faces
+            // here pushed the kernel to 255 registers with spills: the y rows are copied instead.)
+            constexpr int W = 32 / (int)sizeof(T);
+            const long long sh = x < W ? (long long)g.nx : (x >= g.nx - W ? -(long long)g.nx : 0);
+            if (sh != 0) {
+#pragma unroll
+              for (int q = 0; q < NF; ++q) out.f[q][gidx + sh] = lane_of(fn[q], c);
+            }
           }
-        }
-      } else {
-        const long long n = (long long)g.nx * g.ny * g.nz;
-        const long long li = ((long long)o * g.ny + y) * g.nx + x;
+        } else {
+          const long long n = (long long)g.nx * g.ny * g.nz;
+          const long long li = ((long long)o * g.ny + yc) * g.nx + x;
 #pragma unroll
-        for (int q = 0; q < NF; ++q) rhs_out[q * n + li] = rhs[q];
+          for (int q = 0; q < NF; ++q) rhs_out[q * n + li] = lane_of(rhs[q], c);
+        }
       }
     }
 #pragma unroll
@@ -320,7 +367,8 @@ __device__ __forceinline__ void unroll_phases(F&& f, int p, int ze) {
 
 template <typename T, int RAD, int MODE>
 __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
-    zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r, const __grid_constant__ Coef<T> C,
+    zmarch_kernel(const __grid_constant__ TmapSet tm, Fields<T> out, Geom g, Region r,
+                  const __grid_constant__ Coef<typename ZCfg<T, RAD>::V> C,
                   int k, T* __restrict__ rhs_out, int nzc, int xo, int persist) {
   using Z = ZCfg<T, RAD>;
   constexpr int TX = Z::TX, TY = Z::TY;
@@ -349,7 +397,9 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
   // count base + (P - first).
   auto segment = [&](const int x0, const int y0, const int zb, const int ze, const unsigned base) {
     const int x = x0 + tx, y = y0 + ty;
-    const bool active = x < r.lo[0] + r.ext[0] && y < r.lo[1] + r.ext[1];
+    bool active[Z::CPT];
+#pragma unroll
+    for (int c = 0; c < Z::CPT; ++c) active[c] = x < r.lo[0] + r.ext[0] && y + c * Z::RS < r.lo[1] + r.ext[1];
     const int first = zb - RAD;
     const int xs = (x0 - RAD) & ~(Z::CH - 1);  // 16-byte aligned box starts (interior origin is 128-B aligned)
     const int pxs = x0 & ~(Z::CH - 1);
@@ -378,13 +428,13 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
 
     const ZStep<T, RAD, MODE> S{ring, prevbuf, C, (ty + RAD) * Z::COLS + (x - xs), ty * Z::PCOLS + (x - pxs),
                                         first - (int)(base % Z::NSLOT), lead};
-    March<T, RAD> st;
+    March<typename Z::V, RAD> st;
 #pragma unroll
     for (int v = 0; v < 2; ++v)
 #pragma unroll
       for (int j = 0; j < RAD; ++j)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (T)0;
+        for (int c = 0; c < 3; ++c) st.acc[v][j][c] = (typename Z::V)0;
 
     if (tid == 0)
       for (int P = first; P <= zb && P <= ze + RAD - 1; ++P) issue(P);
@@ -443,6 +493,54 @@ __global__ void __launch_bounds__(ZCfg<T, RAD>::NT, 1)
 
 constexpr int kNZC = 64;
 
+// The coefficients in the kernel's compute type (two-cell FP32: every constant broadcast to both lanes).
+template <typename V, typename T>
+Coef<V> coef_as(const Coef<T>& c) {
+  if constexpr (std::is_same<V, T>::value) {
+    return c;
+  } else {
+    Coef<V> o;
+    auto cv = [](T x) { return V((double)x); };
+    for (int a = 0; a < 3; ++a) {
+      for (int i = 0; i < RMAX; ++i) {
+        o.c1[a][i] = cv(c.c1[a][i]);
+        o.d2[a][i] = cv(c.d2[a][i]);
+        o.xw[a][i] = cv(c.xw[a][i]);
+      }
+      o.d0[a] = cv(c.d0[a]);
+      o.rkA[a] = cv(c.rkA[a]);
+      o.rkB[a] = cv(c.rkB[a]);
+    }
+#define B2_CV(f) o.f = cv(c.f)
+    B2_CV(gamma_cp); B2_CV(gm1); B2_CV(inv_cp); B2_CV(lnrho0); B2_CV(cs0sq); B2_CV(inv_T0); B2_CV(H_C);
+    B2_CV(eta_inv_mu0); B2_CV(inv_mu0); B2_CV(nu); B2_CV(nu3); B2_CV(two_nu); B2_CV(zeta); B2_CV(eta); B2_CV(K);
+#undef B2_CV
+    return o;
+  }
+}
+
+// z chunk of a whole-grid launch (zchunk < 0): the chunk count per tile column that minimises
+// (waves of `resident` CTAs) x (planes per CTA, the 2r prologue planes counted at half cost), so
+// that the last wave is not left mostly empty.  E.g. 256^3 FP64 (256 columns, 148 resident CTAs):
+// 4 chunks of 64 (6.9 waves); FP32 (128 columns of the 32 x 16 tile): 8 chunks of 32 (6.9 waves)
+// instead of 4 of 64 (3.5 waves: the fourth wave half empty; measured 24.6 vs 22.3 Gcell/s).
+inline int balanced_zchunk(int columns, int nz, int rad, int resident) {
+  double best = 1e300;
+  int arg = std::min(nz, kNZC);
+  for (int c = 1; c <= nz; ++c) {
+    const int len = (nz + c - 1) / c;
+    if (len < 2 * rad || len > 4 * kNZC) continue;
+    const long long ctas = (long long)columns * ((nz + len - 1) / len);
+    const long long waves = (ctas + resident - 1) / resident;
+    const double t = (double)waves * (len + rad);
+    if (t < best - 1e-9) {
+      best = t;
+      arg = len;
+    }
+  }
+  return arg;
+}
+
 template <typename T, int RAD, int MODE>
 void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const Geom& g, const Region& r,
                 const Coef<T>& C, int k, T* rhs_out, int xo, bool persist, int zchunk) {
@@ -454,6 +552,10 @@ void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const 
   cudaGetDevice(&dev);
   int& resident = resident_of[dev & 63];
   if (!resident) {
+    if constexpr (std::is_same<typename Z::V, F2>::value) {
+      const float2 nz = make_float2(-0.0f, -0.0f);  // the opaque addend of F2 products (mhd_math.cuh)
+      cudaMemcpyToSymbol(b2_f2_nz, &nz, sizeof(nz));
+    }
     cudaFuncSetAttribute(zmarch_kernel<T, RAD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Z::SMEM);
     int sms = 0, per = 0;
@@ -461,14 +563,18 @@ void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, zmarch_kernel<T, RAD, MODE>, Z::NT, Z::SMEM);
     resident = std::max(1, sms * std::max(1, per));
   }
-  const int cz = zchunk > 0 ? zchunk : kNZC;
+  const int cz = zchunk > 0 ? zchunk : (zchunk < 0 ? balanced_zchunk((r.ext[0] + Z::TX - 1) / Z::TX *
+                                                                      ((r.ext[1] + Z::TY - 1) / Z::TY),
+                                                                  r.ext[2], RAD, resident)
+                                                 : kNZC);
   const int nzc = r.ext[2] < cz ? r.ext[2] : cz;
   dim3 grd((r.ext[0] + Z::TX - 1) / Z::TX, (r.ext[1] + Z::TY - 1) / Z::TY, (r.ext[2] + nzc - 1) / nzc);
   // persistent schedule when the chunked grid would take more than one wave (and the warp-group
   // skew, whose barrier ids follow the plane parity, is off)
   const bool pers = persist && !Z::SKEW && (long long)grd.x * grd.y * grd.z > resident;
   if (pers) grd = dim3(resident, 1, 1);
-  zmarch_kernel<T, RAD, MODE><<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, C, k, rhs_out, nzc, xo, pers ? 1 : 0);
+  zmarch_kernel<T, RAD, MODE>
+      <<<grd, Z::NT, Z::SMEM, st>>>(tm, out, g, r, coef_as<typename Z::V>(C), k, rhs_out, nzc, xo, pers ? 1 : 0);
 }
 
 }  // namespace zm
