@@ -638,9 +638,10 @@ void update_region_r(mhd_mesh* m, cudaStream_t st, const Region& r, int k, doubl
   const double cells = (double)r.ext[0] * r.ext[1] * r.ext[2];
   PhaseTimer t(m, st, st == m->stream ? MHD_PHASE_UPDATE : MHD_PHASE_OUTER,
                cells * NF * sizeof(T) * (rhs_out ? 2.0 : (k == 0 ? 2.0 : 3.0)));
-  // main stream: wave-balanced z chunks (B2MHD_ZCHUNK overrides); boundary slabs: 16 (FP32) / 64
+  // main stream: wave-balanced z chunks (B2MHD_ZCHUNK overrides); boundary slabs: 16 (FP32) / 32
+  // (FP64: 50.6 vs 49.2 Gcell/s with 64 at 4 GPUs weak, profiles/r02/mgpu/slabc_*)
   const int zchunk = st == m->stream ? m->zchunk_env
-                                     : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 0));
+                                     : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 32));
   bool done = false;
   if constexpr (std::is_same<T, double>::value && RAD == 3) {
     // warp-specialised variant (zsplit.cuh): variant 3, or variant 0 when enabled for the mesh
