@@ -58,11 +58,11 @@ def test_multigpu_fp32(nproc, exchange):
 
 @pytest.mark.parametrize("nproc", [2, 4, 8])
 def test_multigpu_full_size_bit_identity(nproc):
-    """BASELINE's 512^3 strong-scaling grid in bench.py's launch configuration (auto exchange):
+    """BASELINE's 512^3 strong-scaling grid in bench.py's launch configuration (peer memory):
     every rank's state after one RK3 step equals the same region of a 1-GPU 512^3 run, bitwise."""
     if _ngpus() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
-    env = dict(os.environ, MGPU_N="512,512,512", MGPU_EXCHANGE="p2p" if nproc in (2, 4) else "nccl")
+    env = dict(os.environ, MGPU_N="512,512,512", MGPU_EXCHANGE="p2p")  # bench.py's default at every N
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", f"--master-port={29580 + nproc}", os.path.join(ROOT, "tools", "mgpu_full.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
