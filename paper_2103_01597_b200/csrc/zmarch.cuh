@@ -69,11 +69,13 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
-// The centres of plane o + 1, loaded from the ring as the first z taps of output o, are kept in
-// registers and reused as the centres of output o + 1 (8 LDS per cell fewer, +12 registers;
-// 13.36 vs 13.30 Gcell/s, profiles/r02/next_*).
+// B2_ZM_NEXT=1 (build option): the centres of plane o + 1, loaded from the ring as the first z taps
+// of output o, are kept in registers and reused as the centres of output o + 1 (8 LDS per cell
+// fewer, 252 instead of 240 registers).  One GPU: 13.36 vs 13.30 Gcell/s; 4 GPUs weak: 47.7-49.9
+// vs 50.6 (the boundary slabs and the inner launch interleave worse), so it is off
+// (profiles/r02/next_*, mgpu/next_*).
 #ifndef B2_ZM_NEXT
-#define B2_ZM_NEXT 1
+#define B2_ZM_NEXT 0
 #endif
 #ifndef B2_ZM_F32_CPT
 #define B2_ZM_F32_CPT 1
