@@ -323,7 +323,7 @@ struct mhd_mesh {
   int cur = 0;
   int next_k = 0;
   int variant = 0;
-  bool split = false;  // variant 0: use the warp-specialised z-march where supported (B2MHD_ZSPLIT)
+  int split_env = -1;  // variant 0: warp-specialised z-march (B2MHD_ZSPLIT=0/1; -1: per-radius default)
   // peer-memory substeps: each boundary slab waits only for the neighbours whose halo it reads
   // (B2MHD_FINE_ARRIVAL=0: one wait for every neighbour before the first slab, the round-1 schedule)
   bool fine_arrival = true;
@@ -643,9 +643,11 @@ void update_region_r(mhd_mesh* m, cudaStream_t st, const Region& r, int k, doubl
   const int zchunk = st == m->stream ? m->zchunk_env
                                      : (m->slab_zchunk >= 0 ? m->slab_zchunk : (sizeof(T) == 4 ? 16 : 32));
   bool done = false;
-  if constexpr (std::is_same<T, double>::value && RAD == 3) {
+  if constexpr (std::is_same<T, double>::value && (RAD == 3 || RAD == 4)) {
     // warp-specialised variant (zsplit.cuh): variant 3, or variant 0 when enabled for the mesh
-    if (zm && (m->variant == 3 || (m->variant == 0 && m->split)) && zsplit_supported<T, RAD>(m->g, r)) {
+    // (B2MHD_ZSPLIT; default on for radius 4, where it doubles the warps per SM)
+    const bool want = m->variant == 3 || (m->variant == 0 && (m->split_env >= 0 ? m->split_env != 0 : RAD == 4));
+    if (zm && want && zsplit_supported<T, RAD>(m->g, r)) {
       launch_zsplit<T, RAD>(st, m->tmaps[m->cur], out, m->g, r, C, k, rhs_out, (int)m->L.xo, zchunk);
       done = true;
     }
@@ -1282,7 +1284,7 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   m->info = *info;
   if (const char* w = getenv("B2MHD_XWRAP")) m->xwrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_PERSIST")) m->persist_env = atoi(w) != 0;
-  if (const char* w = getenv("B2MHD_ZSPLIT")) m->split = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_ZSPLIT")) m->split_env = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_FINE_ARRIVAL")) m->fine_arrival = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_SLAB_ZCHUNK")) m->slab_zchunk = atoi(w);
   if (const char* w = getenv("B2MHD_ZCHUNK")) m->zchunk_env = atoi(w);
@@ -1582,8 +1584,10 @@ mhd_status mhd_set_kernel(mhd_mesh* m, int32_t variant) {
     Region full = {{0, 0, 0}, {m->g.nx, m->g.ny, m->g.nz}};
     const bool ok = m->tmaps_ok && (m->info.dtype == MHD_F64 ? zmarch_ok<double>(m, full) : zmarch_ok<float>(m, full));
     if (!ok) return fail(MHD_EUNSUPPORTED, "z-marching kernel does not support this geometry");
-    if (variant == 3 && !(m->info.dtype == MHD_F64 && m->info.radius == 3 && zsplit_supported<double, 3>(m->g, full)))
-      return fail(MHD_EUNSUPPORTED, "the warp-specialised kernel is FP64, radius 3 only");
+    if (variant == 3 && !(m->info.dtype == MHD_F64 &&
+                          ((m->info.radius == 3 && zsplit_supported<double, 3>(m->g, full)) ||
+                           (m->info.radius == 4 && zsplit_supported<double, 4>(m->g, full)))))
+      return fail(MHD_EUNSUPPORTED, "the warp-specialised kernel is FP64, radius 3 or 4 only");
   }
   m->variant = variant;
   return MHD_OK;

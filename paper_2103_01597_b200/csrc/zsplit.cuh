@@ -122,7 +122,9 @@ struct SCfg {
   // slower, the pointwise global loads exposed; profiles/r02/split3_*.)
   static constexpr int NSLOT = RAD + 2;
   static constexpr size_t SMEM = (size_t)(NSLOT * Z::SLOT + 2 * NF * Z::PSZ) * Z::ES + 128;
-  static constexpr bool OK = sizeof(T) == 8 && Z::NT == 256 && !Z::SKEW && SMEM <= 227 * 1024;
+  // 32 x 8 tiles (512 threads, registers rebalanced by setmaxnreg) and the 32 x 4 tiles of radius 4
+  // (256 threads: every thread may use 255 registers, 8 warps per SM instead of 4)
+  static constexpr bool OK = sizeof(T) == 8 && (Z::NT == 256 || Z::NT == 128) && SMEM <= 227 * 1024;
 };
 
 template <typename T, int RAD, int MODE>
@@ -520,10 +522,10 @@ __global__ void __launch_bounds__(SCfg<T, RAD>::NT, 1)
     for (int P = X.first; P <= X.last && P < X.first + NSLOT; ++P) X.issue(P);
 
   if (grp == 0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_MAG));
+    if constexpr (S::NT == 512) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_MAG));
     group_march<T, RAD, MODE, 0>(X, ct, lane, tq);
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_FLOW));
+    if constexpr (S::NT == 512) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_FLOW));
     group_march<T, RAD, MODE, 1>(X, ct, lane, tq);
   }
 

@@ -467,20 +467,22 @@ def test_paper_ulp_analog_256():
 # ---- stencil orders 2, 4, 6, 8 -------------------------------------------------------------
 @pytest.mark.parametrize("r", [1, 2, 3, 4])
 def test_orders_rhs_steps_and_kernels(r):
-    """Every order: RHS parity, 3 RK3 steps parity, and the direct and z-marching kernels agree
-    bit for bit (FP64 radius 4 runs on the direct kernel only: its ring does not fit in smem)."""
+    """Every order: RHS parity, 3 RK3 steps parity, and the direct, z-marching and (radius 3, 4)
+    warp-specialised kernels agree bit for bit."""
     import paper_2103_01597_b200 as b2
     from paper_2103_01597_b200 import MhdError
     n = (40, 28, 24)
     ds = synth.spacing(n)
     st = synth.pcg64_state((n[2], n[1], n[0]))
     outs = []
-    for variant in (1, 2):
+    for variant in (1, 2, 3):
         m, _ = _mesh(n, ds, PSTRONG, radius=r)
         try:
             m.set_kernel(variant)
         except MhdError:
-            assert variant == 2 and r == 4
+            # z-march single group at FP64 radius 4 runs on a 32 x 4 tile; the warp-specialised
+            # kernel exists for radius 3 and 4 only
+            assert (variant == 2 and r == 4) or (variant == 3 and r < 3)
             m.close()
             continue
         m.load(st)
@@ -495,8 +497,8 @@ def test_orders_rhs_steps_and_kernels(r):
     for o in outs:
         assert _field_err(o, ref) <= 1e-11
         assert _norm_err(o - st, ref - st) <= 1e-9
-    if len(outs) == 2:
-        assert np.array_equal(outs[0], outs[1])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
 
 
 @pytest.mark.parametrize("r", [1, 2, 3, 4])
