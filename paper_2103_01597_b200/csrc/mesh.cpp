@@ -203,6 +203,13 @@ Coef<T> make_coef(const mhd_mesh_info& info, int k, double dt) {
   C.zeta = (T)ph.zeta;
   C.eta = (T)ph.eta;
   C.K = (T)ph.K;
+  for (int i = 0; i < RMAX; ++i)
+    for (int a = 0; a < 2; ++a) {
+      C.xy_c1[i][a] = C.c1[a][i];
+      C.xy_d2[i][a] = C.d2[a][i];
+    }
+  C.xy_d0[0] = C.d0[0];
+  C.xy_d0[1] = C.d0[1];
   // Williamson (1980) 2N RK3 (R#3)
   const double alpha[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
   const double beta[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};

@@ -30,6 +30,10 @@ struct Coef {
   T gamma_cp, gm1, inv_cp, lnrho0, cs0sq, inv_T0, H_C, eta_inv_mu0, inv_mu0, nu, nu3, two_nu, zeta, eta, K;
   // RK3 update: f_{k+1} = f_k + rkA[k] (f_k - f_{k-1}) + rkB[k] RHS  (R#3, R#4)
   T rkA[3], rkB[3];
+  // (x, y) pairs of the in-plane weights, for paired FP32x2 evaluation of the x and y axes
+  alignas(2 * sizeof(T)) T xy_c1[RMAX][2];
+  alignas(2 * sizeof(T)) T xy_d2[RMAX][2];
+  alignas(2 * sizeof(T)) T xy_d0[2];
 };
 
 // All derivative quantities one cell needs.

@@ -74,6 +74,10 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
 // fewer, 252 instead of 240 registers).  One GPU: 13.36 vs 13.30 Gcell/s; 4 GPUs weak: 47.7-49.9
 // vs 50.6 (the boundary slabs and the inner launch interleave worse), so it is off
 // (profiles/r02/next_*, mgpu/next_*).
+// FP32: the x and y axes of axis_xy evaluated as FP32x2 pairs (FFMA2 / FADD2)
+#ifndef B2_ZM_F32_XY2
+#define B2_ZM_F32_XY2 1
+#endif
 #ifndef B2_ZM_NEXT
 #define B2_ZM_NEXT 0
 #endif
@@ -180,6 +184,35 @@ struct ZStep {
   // x/y first and second derivatives of field q in the slot, with the differences kept
   __device__ __forceinline__ void axis_xy(const T* sp, int q, V f0, V (&d1)[2], V (&d2)[2], V (&dlx)[RAD],
                                           V (&dly)[RAD]) const {
+#if B2_ZM_F32_XY2
+    if constexpr (std::is_same<V, float>::value) {
+      // FP32: the x and y axes as the two lanes of FP32x2 instructions, each lane the same
+      // operations in the same order as d1_of / d2_of (bit-identical to the scalar path)
+      float2 dl[RAD], sg[RAD];
+#pragma unroll
+      for (int i = 1; i <= RAD; ++i) {
+        const float2 pp = make_float2(at(sp, q, i, 0), at(sp, q, 0, i));
+        const float2 mm = make_float2(at(sp, q, -i, 0), at(sp, q, 0, -i));
+        dl[i - 1] = __fadd2_rn(pp, make_float2(-mm.x, -mm.y));
+        sg[i - 1] = __fadd2_rn(pp, mm);
+        dlx[i - 1] = dl[i - 1].x;
+        dly[i - 1] = dl[i - 1].y;
+      }
+      const float2* c1 = reinterpret_cast<const float2*>(C.xy_c1);
+      const float2* dd = reinterpret_cast<const float2*>(C.xy_d2);
+      float2 a = __ffma2_rn(c1[0], dl[0], b2_f2_nz);  // the product, opaque to contraction
+#pragma unroll
+      for (int i = 1; i < RAD; ++i) a = __ffma2_rn(c1[i], dl[i], a);
+      float2 b = __ffma2_rn(*reinterpret_cast<const float2*>(C.xy_d0), make_float2(f0, f0), b2_f2_nz);
+#pragma unroll
+      for (int i = 0; i < RAD; ++i) b = __ffma2_rn(dd[i], sg[i], b);
+      d1[0] = a.x;
+      d1[1] = a.y;
+      d2[0] = b.x;
+      d2[1] = b.y;
+      return;
+    }
+#endif
     V sgx[RAD], sgy[RAD];
 #pragma unroll
     for (int i = 1; i <= RAD; ++i) {
@@ -542,6 +575,13 @@ Coef<V> coef_as(const Coef<T>& c) {
       o.rkA[a] = cv(c.rkA[a]);
       o.rkB[a] = cv(c.rkB[a]);
     }
+    for (int i = 0; i < RMAX; ++i)
+      for (int a = 0; a < 2; ++a) {
+        o.xy_c1[i][a] = cv(c.xy_c1[i][a]);
+        o.xy_d2[i][a] = cv(c.xy_d2[i][a]);
+      }
+    o.xy_d0[0] = cv(c.xy_d0[0]);
+    o.xy_d0[1] = cv(c.xy_d0[1]);
 #define B2_CV(f) o.f = cv(c.f)
     B2_CV(gamma_cp); B2_CV(gm1); B2_CV(inv_cp); B2_CV(lnrho0); B2_CV(cs0sq); B2_CV(inv_T0); B2_CV(H_C);
     B2_CV(eta_inv_mu0); B2_CV(inv_mu0); B2_CV(nu); B2_CV(nu3); B2_CV(two_nu); B2_CV(zeta); B2_CV(eta); B2_CV(K);
@@ -583,8 +623,8 @@ void launch_cfg(cudaStream_t st, const TmapSet& tm, const Fields<T>& out, const 
   cudaGetDevice(&dev);
   int& resident = resident_of[dev & 63];
   if (!resident) {
-    if constexpr (std::is_same<typename Z::V, F2>::value) {
-      const float2 nz = make_float2(-0.0f, -0.0f);  // the opaque addend of F2 products (mhd_math.cuh)
+    if constexpr (sizeof(T) == 4) {
+      const float2 nz = make_float2(-0.0f, -0.0f);  // the opaque addend of FP32x2 products (mhd_math.cuh)
       cudaMemcpyToSymbol(b2_f2_nz, &nz, sizeof(nz));
     }
     cudaFuncSetAttribute(zmarch_kernel<T, RAD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
