@@ -112,6 +112,25 @@ def test_group_steps_bit_identical_and_oracle(nranks, exchange):
     assert _field_err(got, ref) <= 1e-11
 
 
+@pytest.mark.parametrize("nranks", [4, 8])
+def test_group_p2p_coarse_arrival_same_bits(nranks, monkeypatch):
+    """The round-1 peer-memory schedule (one wait for every neighbour before the first boundary
+    slab, B2MHD_FINE_ARRIVAL=0) and the per-slab arrival schedule give the same bits."""
+    import paper_2103_01597_b200 as b2
+    N = GRID[nranks]
+    st = synth.pcg64_state((N[2], N[1], N[0]))
+    outs = []
+    for fine in ("0", "1"):
+        monkeypatch.setenv("B2MHD_FINE_ARRIVAL", fine)
+        g = _group(N, nranks, "p2p", debug=b2.MHD_DEBUG_POISON_HALO)
+        g.load(st)
+        for _ in range(2):
+            g.step(synth.DT)
+        outs.append(g.store())
+        g.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("exchange", ["packed", "p2p"])
 def test_group_corners_on_same_result(exchange):
     """Exchanging the corner segments changes nothing (Eq. 14 has no 3-D corner points)."""
