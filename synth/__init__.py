@@ -55,18 +55,21 @@ def _splitmix64(x: np.ndarray) -> np.ndarray:
         return z ^ (z >> np.uint64(31))
 
 
-def splitmix_state(global_zyx, lo_zyx, n_zyx, seed: int = SEED, dtype=np.float64) -> np.ndarray:
+def splitmix_state(global_zyx, lo_zyx, n_zyx, seed: int = SEED, dtype=np.float64, fields=None) -> np.ndarray:
     """Counter-based ICs for the block [lo, lo+n) of a global grid: value(field q, global linear
-    index g) = (splitmix64(seed ^ (q * C_N + g)) >> 11) * 2^-53.  Decomposition independent."""
+    index g) = (splitmix64(seed ^ (q * C_N + g)) >> 11) * 2^-53.  Decomposition independent.
+    fields: the field indices to generate (default all 8), in that order."""
     Nz, Ny, Nx = global_zyx
     cn = np.uint64(Nz * Ny * Nx)
     z = np.arange(lo_zyx[0], lo_zyx[0] + n_zyx[0], dtype=np.uint64)[:, None, None]
     y = np.arange(lo_zyx[1], lo_zyx[1] + n_zyx[1], dtype=np.uint64)[None, :, None]
     x = np.arange(lo_zyx[2], lo_zyx[2] + n_zyx[2], dtype=np.uint64)[None, None, :]
     gidx = (z * np.uint64(Ny) + y) * np.uint64(Nx) + x
-    out = np.empty((NF,) + tuple(n_zyx), dtype=dtype)
+    fields = tuple(range(NF)) if fields is None else tuple(fields)
+    out = np.empty((len(fields),) + tuple(n_zyx), dtype=dtype)
     with np.errstate(over="ignore"):
-        for q in range(NF):
-            h = _splitmix64(np.uint64(seed) ^ (np.uint64(q) * cn + gidx))
-            out[q] = ((h >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)).astype(dtype)
+        for i, q in enumerate(fields):
+            for z0 in range(0, int(n_zyx[0]), 64):  # z slabs bound the temporaries
+                h = _splitmix64(np.uint64(seed) ^ (np.uint64(q) * cn + gidx[z0:z0 + 64]))
+                out[i, z0:z0 + 64] = ((h >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)).astype(dtype)
     return out

@@ -67,3 +67,19 @@ def test_multigpu_full_size_bit_identity(nproc):
            "--master-addr", "127.0.0.1", f"--master-port={29580 + nproc}", os.path.join(ROOT, "tools", "mgpu_full.py")]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)
     assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+
+
+def test_multigpu_1024_checksum_identity():
+    """BASELINE configs[4] (1024^3 FP64) on 4 B200s in bench.py's configuration: every rank's state
+    after one RK3 step has the same bit-sensitive checksums as the same block of a 1-GPU 1024^3 run
+    (137 GB of mesh workspace on one GPU).  Long (host-side ICs of 68 GB): opt in with
+    B2MHD_TEST_1024=1."""
+    if _ngpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    if os.environ.get("B2MHD_TEST_1024") != "1":
+        pytest.skip("opt in with B2MHD_TEST_1024=1 (profiles/r02/mgpu/full1024_4gpu_vs_1gpu.json)")
+    env = dict(os.environ, MGPU_N="1024,1024,1024", MGPU_EXCHANGE="p2p", MGPU_CHECKSUM="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", "--master-port=29592", os.path.join(ROOT, "tools", "mgpu_full.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=3000)
+    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]

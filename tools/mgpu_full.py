@@ -18,6 +18,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def checksum(t):
+    """Bit-sensitive digest of a float64 tensor block: wrapping int64 sums of the bit patterns and
+    of a position-mixed hash of them (any flipped bit changes it, barring a 2^-64 collision)."""
+    import torch
+    b = t.contiguous().view(torch.int64).flatten()
+    idx = torch.arange(b.numel(), device=b.device, dtype=torch.int64)
+    mixed = (b ^ (b >> 29)) * -7046029254386353131 + idx * 0x632BE59BD9B4E019  # odd constants
+    return (int(b.sum().item()), int((mixed ^ (mixed >> 31)).sum().item()))
+
+
 def main():
     import torch
     import torch.distributed as dist
@@ -50,6 +60,46 @@ def main():
     res = {"N": N, "world": world, "exchange": exchange, "steps": steps, "local": [nx, ny, nz]}
     los = [None] * world
     dist.all_gather_object(los, lo)
+    if os.environ.get("MGPU_CHECKSUM") == "1":
+        # grids whose whole 1-GPU state cannot also be held as a copy (1024^3: 137 GB of mesh
+        # workspace on one B200): compare bit-sensitive checksums of every rank's block per field
+        sums = [checksum(mine[q]) for q in range(8)]
+        del mine, mesh  # free this rank's workspace before rank 0 builds the 1-GPU mesh
+        torch.cuda.empty_cache()
+        allsums = [None] * world
+        dist.all_gather_object(allsums, sums)
+        if rank == 0:
+            single = b2.Mesh(N, ds, synth.P0, b2.MHD_F64)
+            for q in range(8):  # one field at a time on the host (8.6 GB each at 1024^3)
+                f = synth.splitmix_state(Nzyx, (0, 0, 0), Nzyx, fields=(q,))[0]
+                b2._native.mhd_load(single.handle, q, f.ctypes.data, b2.MHD_F64, False)
+                del f
+            single.synchronize()
+            for _ in range(steps):
+                single.step(synth.DT)
+            res["ranks_identical"] = [True] * world
+            buf = torch.empty(Nzyx, dtype=torch.float64, device="cuda")
+            finite = True
+            for q in range(8):
+                b2._native.mhd_store(single.handle, q, buf.data_ptr(), b2.MHD_F64, True)
+                torch.cuda.synchronize()
+                finite &= bool(torch.isfinite(buf).all().item())
+                for r in range(world):
+                    z0, y0, x0 = los[r]
+                    same = checksum(buf[z0:z0 + nz, y0:y0 + ny, x0:x0 + nx]) == allsums[r][q]
+                    res["ranks_identical"][r] &= same
+                    ok &= same
+            single.close()
+            res["finite"] = finite
+            res["mode"] = "checksums (sum of the int64 bit patterns and of a mixed hash, per rank and field)"
+            ok &= finite
+        res["ok"] = bool(ok)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        flag = torch.tensor([1 if ok else 0], device="cuda")
+        dist.broadcast(flag, src=0)
+        dist.destroy_process_group()
+        sys.exit(0 if flag.item() == 1 else 1)
     if rank == 0:
         single = b2.Mesh(N, ds, synth.P0, b2.MHD_F64)
         single.load(torch.from_numpy(synth.splitmix_state(Nzyx, (0, 0, 0), Nzyx)))
