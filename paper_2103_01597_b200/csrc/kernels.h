@@ -95,8 +95,11 @@ constexpr int zm_tx() { return 32; }
 #ifndef B2_ZM_TY_F32
 #define B2_ZM_TY_F32 16
 #endif
+#ifndef B2_ZM_TY_F64
+#define B2_ZM_TY_F64 8
+#endif
 template <typename T, int RAD = 3>
-constexpr int zm_ty() { return sizeof(T) == 8 ? (RAD >= 4 ? 4 : 8) : (RAD == 3 ? B2_ZM_TY_F32 : 8); }
+constexpr int zm_ty() { return sizeof(T) == 8 ? (RAD >= 4 ? 4 : B2_ZM_TY_F64) : (RAD == 3 ? B2_ZM_TY_F32 : 8); }
 template <typename T>
 constexpr int zm_ch() { return 16 / (int)sizeof(T); }
 template <typename T, int RAD>

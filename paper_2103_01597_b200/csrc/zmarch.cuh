@@ -78,6 +78,9 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
 #ifndef B2_ZM_F32_XY2
 #define B2_ZM_F32_XY2 1
 #endif
+#ifndef B2_ZM_SKEW_ALL
+#define B2_ZM_SKEW_ALL 0  // build option: the warp-group skew on every tile (measured slower at 8 warps)
+#endif
 #ifndef B2_ZM_NEXT
 #define B2_ZM_NEXT 0
 #endif
@@ -119,7 +122,7 @@ struct ZCfg {
   static constexpr unsigned PREV_TX = (unsigned)(NF * TY * PCOLS * ES);
   static constexpr size_t SMEM = (size_t)(NSLOT * SLOT + 2 * NF * PSZ) * ES + 128 + 16;
   static constexpr bool FITS = SMEM <= 227 * 1024;
-  static constexpr bool SKEW = TY < 8;  // the 4-row tiles (FP64, r = 4)
+  static constexpr bool SKEW = TY < 8 || B2_ZM_SKEW_ALL;  // the 4-row tiles (FP64, r = 4)
   using V = typename ZVal<CPT, T>::type;  // compute type: T, or two FP32 cells (F2)
 };
 
