@@ -410,6 +410,28 @@ def test_full_size_256_rhs_and_substep():
     m.close()
 
 
+def test_full_size_512_rhs_and_substep():
+    """512^3 FP64 on one GPU (BASELINE configs[2] at N = 1, 17.8 GB of state) in bench.py's launch
+    configuration: the RHS of every cell and one substep k = 0 against the oracle on the host cores
+    (≈ 50 GB of host memory)."""
+    import os
+    oracle.set_threads(os.cpu_count() or 1)
+    n = (512, 512, 512)
+    ds = synth.spacing(n)
+    m, _ = _mesh(n, ds)
+    st = synth.splitmix_state((512, 512, 512), (0, 0, 0), (512, 512, 512))
+    m.load(st)
+    got_rhs = m.debug_rhs().cpu().numpy()
+    ref, ref_rhs = oracle.integrate(st, ds, synth.P0, synth.DT, 0, substeps=1, return_rhs=True)
+    assert _norm_err(got_rhs, ref_rhs) <= 1e-12
+    del got_rhs, ref_rhs
+    m.substep(0, synth.DT)
+    got = m.store().cpu().numpy()
+    m.close()
+    assert _field_err(got, ref) <= 1e-11
+    assert _norm_err(got - st, ref - st) <= 1e-10
+
+
 def test_paper_ulp_analog_256():
     """The paper's own verification: one RK3 step of a 256^3 grid of random [0, 1]
     values against the single-core CPU model, error in ulps of the model value (Eqs. 15-16,
