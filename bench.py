@@ -481,6 +481,18 @@ def main():
             line["roofline_substep"]["frac"] = line["roofline_substep"]["achieved"] / line["roofline_substep"]["peak"]
             line["model"] = perf_model(n_glob, world, P, local_cells, substep_ms, prof, args.order // 2,
                                        NF_BYTES[args.dtype])
+        if dtype == b2.MHD_F32 and up["ms"] > 0:
+            # FP32: the same canonical arithmetic as FP64 (mhd_math.cuh), so the same executed
+            # operation count per cell (ncu FP64 counters; FP32x2 pairs count two lane-ops); peak
+            # nominal 148 SM x 128 FP32 lanes x 1.965 GHz (not measured)
+            upd_cells = up["bytes"] / (NF_BYTES[args.dtype] * (2 + 3 + 3) / 3)
+            ach = DP_PER_CELL[args.order] * upd_cells / (up["ms"] * 1e-3)
+            peak32 = 148 * 128 * 1.965e9
+            line["roofline_alu_fp32"] = {"bound": "alu", "achieved": ach, "peak": peak32, "unit": "FP32 lane-ops/s",
+                                         "frac": ach / peak32, "ops_per_cell": DP_PER_CELL[args.order],
+                                         "peak_source": "nominal 148 x 128 x 1.965 GHz",
+                                         "note": "the FP32 kernel is bound by the LSU instruction rate "
+                                                 "(DESIGN.md 7), not by the FP32 pipe"}
         if dp_per_cell and up["ms"] > 0:
             # FP64: the kernel is bound by on-chip work (FP64 pipe and shared-memory wavefronts,
             # DESIGN.md 7), not by HBM, so the FP64 roof is the primary one and HBM secondary.
