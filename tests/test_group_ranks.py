@@ -253,3 +253,26 @@ def test_group_substep_order_and_exclusivity():
     assert e.value.status == 1
     g.substep(0, synth.DT)
     g.close()
+
+
+@pytest.mark.parametrize("nranks,exchange", [(1, None), (2, "p2p"), (4, "packed"), (8, "p2p")])
+def test_minimal_subdomains(nranks, exchange):
+    """The degenerate sizes: every subdomain axis n' = 2r + 1 = 7 (the smallest the method allows,
+    n'_i > 2r; the inner segment is then empty along split axes and every update runs on the direct
+    kernel), with every halo cell of an update's output poisoned: 2 RK3 steps against the oracle
+    (R#18) and, for P > 1, bit for bit against one rank."""
+    import paper_2103_01597_b200 as b2
+    P = {1: (1, 1, 1), 2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}[nranks]  # (x, y, z), Morton P:557
+    N = tuple(7 * p for p in P)
+    st = synth.pcg64_state((N[2], N[1], N[0]))
+    one = _single(N, st, 2, synth.DT)
+    ref = oracle.integrate(st, synth.spacing(N), synth.P0, synth.DT, 2)
+    assert _field_err(one, ref) <= 1e-11
+    if nranks > 1:
+        g = _group(N, nranks, exchange, debug=b2.MHD_DEBUG_POISON_HALO)
+        g.load(st)
+        for _ in range(2):
+            g.step(synth.DT)
+        got = g.store()
+        g.close()
+        assert np.array_equal(got, one)
