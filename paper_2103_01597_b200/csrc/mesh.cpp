@@ -332,7 +332,12 @@ struct mhd_mesh {
   int variant = 0;
   int split_env = -1;  // variant 0: warp-specialised z-march (B2MHD_ZSPLIT=0/1; -1: per-radius default)
   // peer-memory substeps: each boundary slab waits only for the neighbours whose halo it reads
-  // (B2MHD_FINE_ARRIVAL=0: one wait for every neighbour before the first slab, the round-1 schedule)
+  // (B2MHD_FINE_ARRIVAL=0: one wait for every neighbour before the first slab, the round-1
+  // schedule).  Default: FP64 only.  The per-slab wait kernels co-reside with FP64 inner CTAs
+  // (240 registers x 256 threads leave room for a small block), but an FP32 inner CTA takes the
+  // whole register file (127 x 512), so each wait kernel then queues for a free SM: 4 GPUs FP32
+  // 83.1 (per-slab) vs 86.9 Gcell/s (one wait); FP64 50.3 vs 50.2 (profiles/r02/mgpu/)
+  int fine_env = -1;
   bool fine_arrival = true;
   int64_t launches = 0;
   double* h_red = nullptr;  // pinned
@@ -1292,7 +1297,8 @@ mhd_status mhd_mesh_create(const mhd_mesh_info* info, void* dev_workspace, size_
   if (const char* w = getenv("B2MHD_XWRAP")) m->xwrap = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_PERSIST")) m->persist_env = atoi(w) != 0;
   if (const char* w = getenv("B2MHD_ZSPLIT")) m->split_env = atoi(w) != 0;
-  if (const char* w = getenv("B2MHD_FINE_ARRIVAL")) m->fine_arrival = atoi(w) != 0;
+  if (const char* w = getenv("B2MHD_FINE_ARRIVAL")) m->fine_env = atoi(w) != 0;
+  m->fine_arrival = m->fine_env >= 0 ? m->fine_env != 0 : info->dtype == MHD_F64;
   if (const char* w = getenv("B2MHD_SLAB_ZCHUNK")) m->slab_zchunk = atoi(w);
   if (const char* w = getenv("B2MHD_ZCHUNK")) m->zchunk_env = atoi(w);
   if (const char* w = getenv("B2MHD_SLAB")) sscanf(w, "%d,%d,%d", &m->slab_env[0], &m->slab_env[1], &m->slab_env[2]);
