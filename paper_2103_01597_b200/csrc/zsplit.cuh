@@ -1,16 +1,18 @@
-// Warp-specialised z-marching update (the FP64 order-6 hot path on sm_100a).
+// Warp-specialised z-marching update (FP64; the default for order 8, an option for order 6).
 //
-// Same staging as zmarch.cuh (TMA ring of r + 2 planes of the 32 x 8 tile with its radius-r halo,
+// Same staging as zmarch.cuh (TMA ring of r + 2 planes of the tile with its radius-r halo,
 // f_{k-1} of the output plane in the same transaction, z column in registers, push/pull z-cross
-// terms), but each cell is served by TWO threads in two warp groups of 8 warps (512 threads, 16
-// warps per SM instead of 8):
-//   group 0 ("magnetic", warps 0-7):  A -> B, mu0 j, lap A (the magnetic contraction of Eq. B.2-B.4),
-//                                     grad lnrho and lap lnrho; then dA/dt (B.4) and the A update;
-//   group 1 ("flow", warps 8-15):     u and s derivatives; then B.1-B.3 and the lnrho, u, s update.
+// terms), but each cell is served by TWO threads in two warp groups: for the 32 x 8 tile of order
+// 6, 2 x 8 warps (512 threads, 16 warps per SM instead of 8, registers rebalanced by setmaxnreg);
+// for the 32 x 4 tile of order 8, 2 x 4 warps (8 warps per SM instead of 4, up to 255 registers
+// each).  Measured: order 8 9.46 vs 6.59 Gcell/s (default); order 6 12.3 vs 13.3.
+//   group 0 ("magnetic"):  A -> B, mu0 j, lap A (the magnetic contraction of Eq. B.2-B.4),
+//                          grad lnrho and lap lnrho; then dA/dt (B.4) and the A update;
+//   group 1 ("flow"):      u and s derivatives; then B.1-B.3 and the lnrho, u, s update.
 // Group 0 hands grad lnrho, lap lnrho and the pointwise factors of mhd_math.cuh::thermo (Lorentz
 // acceleration, ohmic heating, 1/rho, c_s^2, 1/T: 11 values per cell) to group 1 through tensor
 // memory (tcgen05.st / tcgen05.ld, 32x32b: the two threads of a cell sit in the same lane of warps
-// w and w + 8, which share a TMEM lane quadrant), double-buffered by plane parity and ordered by
+// w and w + NWARP/2, which share a TMEM lane quadrant), double-buffered by plane parity and ordered by
 // named barriers.  Each thread carries half the register state of the single-group kernel (the z
 // history and cross accumulators of its own fields), so twice the warps fit; ring slots are
 // released per plane through "empty" mbarriers (one arrival per warp) instead of a CTA barrier,
@@ -20,8 +22,9 @@
 // The march is not unrolled by phase (the z history and the cross accumulators shift by register
 // moves): two groups of r-fold unrolled code did not fit the instruction cache.
 // Every value is produced by the same expressions in the same order as mhd_math.cuh (rhs_rest =
-// visc_parts + thermo + rhs_flow + rhs_induction), so the result is bit-identical to the direct and single-group kernels
-// (tests/test_gpu_parity.py::test_kernel_variants_bit_identical).
+// visc_parts + thermo + rhs_flow + rhs_induction), so the result is bit-identical to the direct and
+// single-group kernels (tests/test_gpu_parity.py::test_kernel_variants_bit_identical,
+// test_orders_rhs_steps_and_kernels).
 #pragma once
 #include "zmarch.cuh"
 
