@@ -308,7 +308,7 @@ constexpr int kBarProd = 1, kBarCons = 3;
 // Registers per thread of each group after setmaxnreg (the kernel starts at 65536 / 512 = 128):
 // the flow group carries the RHS of B.1-B.3, the magnetic group only the contraction and B.4.
 #ifndef B2_ZS_REG_MAG
-#define B2_ZS_REG_MAG 120
+#define B2_ZS_REG_MAG 128  // measured 112 / 120 / 128 / 136: 11.8 / 12.3 / 13.2 / (spills) Gcell/s
 #endif
 #define B2_ZS_REG_FLOW (256 - B2_ZS_REG_MAG)
 
@@ -524,11 +524,18 @@ __global__ void __launch_bounds__(SCfg<T, RAD>::NT, 1)
   if (tid == NC)  // the producer: first thread of the flow group (the last group to release a plane)
     for (int P = X.first; P <= X.last && P < X.first + NSLOT; ++P) X.issue(P);
 
+  // (setmaxnreg: the group giving registers away decreases first; 128 / 128 needs none)
   if (grp == 0) {
-    if constexpr (S::NT == 512) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_MAG));
+    if constexpr (S::NT == 512 && B2_ZS_REG_MAG < 128)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_MAG));
+    if constexpr (S::NT == 512 && B2_ZS_REG_MAG > 128)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_MAG));
     group_march<T, RAD, MODE, 0>(X, ct, lane, tq);
   } else {
-    if constexpr (S::NT == 512) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_FLOW));
+    if constexpr (S::NT == 512 && B2_ZS_REG_FLOW > 128)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_FLOW));
+    if constexpr (S::NT == 512 && B2_ZS_REG_FLOW < 128)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(B2_ZS_REG_FLOW));
     group_march<T, RAD, MODE, 1>(X, ct, lane, tq);
   }
 
