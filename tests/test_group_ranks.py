@@ -276,3 +276,41 @@ def test_minimal_subdomains(nranks, exchange):
         got = g.store()
         g.close()
         assert np.array_equal(got, one)
+
+
+@pytest.mark.parametrize("radius", [1, 2, 4])
+@pytest.mark.parametrize("nranks", [2, 8])
+def test_group_fp32_other_orders(radius, nranks):
+    """FP32 orders 2, 4, 8 on 2 and 8 ranks (peer memory, poisoned halos): P ranks = 1 rank bit for
+    bit, and the oracle within 1e-4 (R#18)."""
+    import paper_2103_01597_b200 as b2
+    N = GRID[nranks]
+    st = synth.pcg64_state((N[2], N[1], N[0]), dtype=np.float32)
+    g = _group(N, nranks, "p2p", dtype=b2.MHD_F32, radius=radius, debug=b2.MHD_DEBUG_POISON_HALO)
+    g.load(st)
+    for _ in range(2):
+        g.step(1e-5)
+    got = g.store()
+    g.close()
+    assert np.array_equal(got, _single(N, st, 2, 1e-5, dtype=b2.MHD_F32, radius=radius))
+    ref = oracle.integrate(st.astype(np.float64), synth.spacing(N), synth.P0, 1e-5, 2, r=radius)
+    assert _field_err(got.astype(np.float64), ref) <= 1e-4
+
+
+@pytest.mark.parametrize("nranks", [2, 8])
+def test_group_warp_specialised_order6(nranks, monkeypatch):
+    """The warp-specialised kernel (B2MHD_ZSPLIT=1) on the boundary slabs and inner segments of a
+    multi-rank order-6 decomposition gives the same bits as the single-group kernel."""
+    import paper_2103_01597_b200 as b2
+    N = GRID[nranks]
+    st = synth.pcg64_state((N[2], N[1], N[0]))
+    outs = []
+    for split in ("0", "1"):
+        monkeypatch.setenv("B2MHD_ZSPLIT", split)
+        g = _group(N, nranks, "p2p", debug=b2.MHD_DEBUG_POISON_HALO)
+        g.load(st)
+        for _ in range(2):
+            g.step(synth.DT)
+        outs.append(g.store())
+        g.close()
+    assert np.array_equal(outs[0], outs[1])
