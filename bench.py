@@ -481,6 +481,19 @@ def main():
             line["roofline_substep"]["frac"] = line["roofline_substep"]["achieved"] / line["roofline_substep"]["peak"]
             line["model"] = perf_model(n_glob, world, P, local_cells, substep_ms, prof, args.order // 2,
                                        NF_BYTES[args.dtype])
+        if dtype == b2.MHD_F64 and args.order == 6 and up["ms"] > 0 and world == 1:
+            # the binding on-chip resource: shared-memory wavefronts of the LSU pipe,
+            # 14.91 per cell-substep (ncu l1tex__data_pipe_lsu_wavefronts_mem_shared over a k = 2
+            # launch / cells, profiles/r02/ncu_zmarch_final.txt; TMA writes not included), 128 B
+            # each, against the measured LDS.64 rate of 127.4 B/clk/SM (profiles/r02/
+            # microbench_mio_fp64.txt) at the SM clock sampled during the timed region
+            upd_cells = up["bytes"] / (NF_BYTES[args.dtype] * (2 + 3 + 3) / 3)
+            sm_mhz = line["clocks"].get("sm_mhz") or 1965
+            ach = 14.91 * 128 * upd_cells / (up["ms"] * 1e-3) / 1e9
+            peak = 127.4 * 148 * sm_mhz * 1e6 / 1e9
+            line["roofline_smem"] = {"bound": "smem", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                     "frac": ach / peak, "wavefronts_per_cell": 14.91,
+                                     "peak_source": "LDS.64 microbenchmark 127.4 B/clk/SM x 148 SM x sampled SM clock"}
         if dtype == b2.MHD_F32 and up["ms"] > 0:
             # FP32: the same canonical arithmetic as FP64 (mhd_math.cuh), so the same executed
             # operation count per cell (ncu FP64 counters; FP32x2 pairs count two lane-ops); peak
